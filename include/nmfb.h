@@ -1,0 +1,204 @@
+/*
+ * nmfb.h -- C ABI of the B200-native alternating-NNLS hot path
+ * (arXiv 1506.08938 anti-lopsided + greedy coordinate-descent NMF).
+ *
+ * Library: paper_1506_08938_b200/libnmfb.so (sm_100a).  Plain pointers,
+ * sizes and status codes only; no torch types.  All device pointers are
+ * caller-owned; every call is ordered on the given CUDA stream (`stream` is a
+ * cudaStream_t passed as void*, NULL = legacy default stream).
+ *
+ * Reference boundary replaced (paths relative to the reference's
+ * pkg/src/nmfkit/):
+ *   nmfb_estep_dense   <- kernels.estep_dense   kernels.py:284-336 (called parallel.py:117-121)
+ *   nmfb_estep_sparse  <- kernels.estep_sparse  kernels.py:223-281 (called parallel.py:110-114)
+ *   nmfb_mstep_rows    <- kernels.mstep_rows    kernels.py:339-378 (called parallel.py:206-209)
+ *   nmfb_nnls_batch    <- kernels._coefficient_solve + _solve_rescaled, batched
+ *                         (kernels.py:38-220); FAIL_NONE kernels.py:27,
+ *                         FASTBREAK_BLOCK kernels.py:35
+ *   nmfb_gram          <- matrix.gram           matrix.py:181-197
+ *   nmfb_rescale       <- nqp.rescale_arrays + parallel._rescale_for_step
+ *                         (nqp.py:116-131, parallel.py:87-91; H = Q + 2*lambda*I at
+ *                         parallel.py:104,196)
+ *   nmfb_gemm_tall     <- the data products G^T X / X F^T of kernels.py:251-258,
+ *                         270-274, 306-313, 325-329 (dense)
+ *   nmfb_csc_linear / nmfb_csr_yt <- the same products for CSC data (sparse)
+ *   nmfb_dense_residual, nmfb_dot, nmfb_objective
+ *                      <- matrix.frobenius_objective / nmf.regularized_objective
+ *                         (matrix.py:227-260, nmf.py:152-165)
+ *
+ * Status codes: NMFB_OK; NMFB_ERR_NUMERIC (a subproblem produced NaN/Inf or
+ * has an unbounded frozen dimension; *fail_index = lowest failing global
+ * index, the reference's returned fail column/row); NMFB_ERR_ARG;
+ * NMFB_ERR_CUDA (see nmfb_last_error()); NMFB_ERR_DEGENERATE (every diagonal
+ * frozen; single-problem solve only, nqp.py:137-141).
+ */
+#ifndef NMFB_H
+#define NMFB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NMFB_OK 0
+#define NMFB_ERR_NUMERIC 1
+#define NMFB_ERR_ARG 2
+#define NMFB_ERR_CUDA 3
+#define NMFB_ERR_DEGENERATE 4
+
+#define NMFB_F32 0
+#define NMFB_F64 1
+
+/* NMFB_MODE_REFERENCE: thread-per-problem kernels in the reference's exact
+ * operation order, no FMA contraction -- bit-identical to the reference in
+ * fp64.  NMFB_MODE_FAST: register-resident warp-group kernels (fp32). */
+#define NMFB_MODE_FAST 0
+#define NMFB_MODE_REFERENCE 1
+
+#define NMFB_FAIL_NONE (-1)      /* kernels.py:27 */
+#define NMFB_FASTBREAK_BLOCK 32  /* kernels.py:35 */
+#define NMFB_MAX_WORKERS 64
+
+int nmfb_version(void);
+const char *nmfb_last_error(void);
+int nmfb_device_sm_count(void);
+
+/* ---------------- reference drop-in shard entry points -------------------
+ * Same arguments and meaning as the numba kernels, on device buffers:
+ *   VT (m, n) C-order, G (n, r), FT (m, r), YT (n, r), HP (r, r) upper
+ *   triangle accumulated (caller mirrors), Qa (ra, ra), scale_a (ra),
+ *   act_idx (ra, int32), active (r, uint8).  dtype of every real array =
+ *   `dtype`.  Solutions overwrite FT / G rows [lo, hi); YT/HP accumulate.
+ * Synchronous: the stream is synchronized before returning the reference's
+ * result tuple (inner_total, max_stop, fail) through host pointers.
+ * Returns NMFB_OK or NMFB_ERR_NUMERIC (then *fail = failing column/row). */
+int nmfb_estep_dense(int dtype, int mode, const void *VT, int64_t m, int64_t n, int64_t col_lo,
+                     int64_t col_hi, const void *G, int32_t r, const void *Qa,
+                     const void *scale_a, const int32_t *act_idx, int32_t ra,
+                     const uint8_t *active, double mu1, double eps, int32_t max_inner,
+                     double max_stop0, void *FT, void *YT, void *HP, int64_t *inner_total,
+                     double *max_stop, int64_t *fail, void *stream);
+
+int nmfb_estep_sparse(int dtype, int mode, const int64_t *indptr, const int32_t *rowidx,
+                      const void *vals, int64_t m, int64_t n, int64_t col_lo, int64_t col_hi,
+                      const void *G, int32_t r, const void *Qa, const void *scale_a,
+                      const int32_t *act_idx, int32_t ra, const uint8_t *active, double mu1,
+                      double eps, int32_t max_inner, double max_stop0, void *FT, void *YT,
+                      void *HP, int64_t *inner_total, double *max_stop, int64_t *fail,
+                      void *stream);
+
+int nmfb_mstep_rows(int dtype, int mode, const void *YT, int64_t row_lo, int64_t row_hi,
+                    const void *Qa, const void *scale_a, const int32_t *act_idx, int32_t ra,
+                    const uint8_t *active, double beta1, double eps, int32_t max_inner,
+                    double max_stop0, void *G, int32_t r, int64_t *inner_total,
+                    double *max_stop, int64_t *fail, void *stream);
+
+/* ---------------- stream-ordered building blocks (async) ---------------- */
+
+/* Batched NNLS over `count` problems with global indices index_base..+count
+ * (fast-break blocks are the 32-aligned runs of global indices; the first
+ * partial block starts from max_stop0, kernels.py:245-248).
+ * Linear terms: h_parts == 0 -> h (count, h_ld) is h itself; else
+ * h = h_base - sum_{s < h_parts} h[s * h_pstride + j * h_ld + i] (the data
+ * products as split-K partials; h_parts == 1 is the reference's
+ * beta1 - YT[row], kernels.py:365).  h_dtype may be F64 with dtype F32.
+ * ra_dev (nullable): device int32 ra written by nmfb_rescale; when given,
+ * Qa is read with leading dimension ra and `ra` is ignored.
+ * stats (device, 2 x uint64): [0] += total inner iterations,
+ * [1] = min(stats[1], lowest failing global index) -- initialise [1] to
+ * UINT64_MAX.  iters_out / final_out (device, nullable): per-problem
+ * iteration count (-1 = failed) and final squared passive-gradient norm.
+ * lanes: lanes per problem for the fast kernel (0 = auto; 1,2,4,8). */
+int nmfb_nnls_batch(int dtype, int mode, const void *Qa, const void *scale_a,
+                    const int32_t *act_idx, const uint8_t *active, int32_t r, int32_t ra,
+                    const int32_t *ra_dev, const void *h, int h_dtype, int32_t h_parts,
+                    int64_t h_ld, int64_t h_pstride, double h_base, void *x, int64_t count,
+                    int64_t index_base, double eps, int32_t max_inner, double max_stop0,
+                    int32_t *iters_out, void *final_out, uint64_t *stats, int32_t lanes,
+                    void *stream);
+
+/* Public single-problem NQP solve (nqp.solve, nqp.py:217-320) for `count`
+ * problems sharing one rescaled Hessian but each with its OWN stop state
+ * (threshold max_stop, no fast-break sharing), fp64, reference order.
+ * hist (nullable, count x hist_ld x 2 doubles): per-iteration squared
+ * passive-gradient norm and rescaled objective, entry 0 = initial. */
+int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_idx,
+                   const uint8_t *active, int32_t r, const int32_t *ra_dev, const double *h,
+                   double *x, int64_t count, double eps, int32_t max_inner, double max_stop,
+                   int32_t *iters_out, double *final_out, double *hist, int32_t hist_ld,
+                   uint64_t *stats, void *stream);
+
+/* Gram A^T A of A (rows, r) row-major (leading dim lda), accumulated in fp64
+ * with a fixed (deterministic) summation order; out = full symmetric r x r
+ * fp64.  workspace: nmfb_gram_workspace_bytes(rows, r) bytes of device mem. */
+size_t nmfb_gram_workspace_bytes(int64_t rows, int32_t r);
+int nmfb_gram(int dtype, const void *A, int64_t rows, int32_t r, int64_t lda, double *out,
+              void *workspace, void *stream);
+
+/* H = G + diag_add * I (G r x r fp64), then the anti-lopsided unit-diagonal
+ * rescale: active = diag > 1e-12 * max diag; scale = sqrt(diag);
+ * Q = H / outer(scale, scale) over active dims.  Writes the compact Qa
+ * (ra x ra, dtype), scale_a (ra, dtype), act_idx (ra), active (r) and the
+ * device scalar ra_dev.  Bit-exact against nqp.rescale_arrays in fp64.
+ * full_scale (nullable, r doubles): sqrt(diag) for every dim. */
+int nmfb_rescale(int dtype, const double *G, int32_t r, double diag_add, void *Qa,
+                 void *scale_a, int32_t *act_idx, uint8_t *active, int32_t *ra_dev,
+                 double *full_scale, void *stream);
+
+/* Split-K tall-skinny GEMM, fp32: C[s] (M x N, row-major, ld N) =
+ * A(M x K) B(K x N) over the s-th K chunk, s < splits.  A(i, k) =
+ * A[i*lda + k] if a_kmajor else A[k*lda + i]; B (K x N) row-major, ld ldb.
+ * C must hold splits*M*N floats.  Deterministic. */
+int nmfb_gemm_tall(const float *A, int a_kmajor, int64_t M, int64_t K, int64_t lda,
+                   const float *B, int32_t N, int64_t ldb, float *C, int32_t splits,
+                   void *stream);
+
+/* Reference-order dense products (check mode), dtype F64 or F32:
+ * h[col - col_lo][i] = mu1 - sum_{row, v != 0} G[row][i] * v, v = VT[col][row]
+ * (kernels.py:306-313).  Cols [col_lo, col_hi). */
+int nmfb_dense_linear_ref(int dtype, const void *VT, int64_t n, int64_t col_lo, int64_t col_hi,
+                          const void *G, int32_t r, double mu1, void *h, void *stream);
+/* YT[row][i] = sum_w ( sum_{col in shard w} x[col][i] * v ) with per-worker
+ * partials summed in worker order (kernels.py:325-329 + parallel.py:150-156).
+ * shard_bounds: host array of workers+1 ascending column bounds. */
+int nmfb_dense_yt_ref(int dtype, const void *VT, int64_t m, int64_t n, const void *FT,
+                      int32_t r, const int64_t *shard_bounds, int32_t workers, void *YT,
+                      void *stream);
+/* H_f[a][b] = sum_w sum_{col in shard w, x_a != 0} x_a x_b, mirrored
+ * (kernels.py:276-280 / 331-335 + parallel.py:127-128, 150-156). */
+int nmfb_hp_ref(int dtype, const void *FT, int64_t m, int32_t r, const int64_t *shard_bounds,
+                int32_t workers, void *HF, void *stream);
+
+/* Sparse products.  CSC (indptr int64 m+1, rowidx int32, vals):
+ * h[col - col_lo][i] = mu1 - sum_t G[rowidx[t]][i] * vals[t]  (kernels.py:251-258)
+ * mode REFERENCE: exact sequential order.  CSR of the same matrix (rowptr
+ * int64 n+1, colidx int32 ascending per row, vals):
+ * YT[row][i] = sum over the row's entries x[col][i] * v, accumulated in
+ * YT's dtype (yt_dtype F64 for the trace-identity objective); REFERENCE mode
+ * emulates the per-worker partial sums of shard_bounds (kernels.py:270-274). */
+int nmfb_csc_linear(int dtype, int mode, const int64_t *indptr, const int32_t *rowidx,
+                    const void *vals, int64_t col_lo, int64_t col_hi, const void *G, int32_t r,
+                    double mu1, void *h, void *stream);
+int nmfb_csr_yt(int dtype, int mode, const int64_t *rowptr, const int32_t *colidx,
+                const void *vals, int64_t n, const void *FT, int32_t r, int yt_dtype,
+                const int64_t *shard_bounds, int32_t workers, void *YT, void *stream);
+
+/* Dense residual 0.5 * ||X - G F||^2 with X given as XT (m, n) row-major,
+ * G (n, r), FT (m, r); fp64 accumulation; result added to *out (device
+ * double) deterministically.  workspace: nmfb_residual_workspace_bytes. */
+size_t nmfb_residual_workspace_bytes(int64_t m, int64_t n);
+int nmfb_dense_residual(int dtype, const void *XT, int64_t m, int64_t n, const void *G,
+                        const void *FT, int32_t r, double *out, void *workspace, void *stream);
+
+/* out[0] = sum a_i * b_i, out[1] = sum |a_i|, out[2] = sum a_i^2 (fp64,
+ * deterministic).  b may be NULL (then out[0] = 0).  a_dtype / b_dtype. */
+size_t nmfb_dot_workspace_bytes(int64_t len);
+int nmfb_dot(const void *a, int a_dtype, const void *b, int b_dtype, int64_t len, double *out,
+             void *workspace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMFB_H */

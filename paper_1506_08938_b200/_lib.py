@@ -1,0 +1,124 @@
+"""ctypes binding of libnmfb.so (the C ABI declared in include/nmfb.h).
+
+There is no fallback: if the library is missing, or no CUDA device is
+present, every entry point raises.  Torch tensors cross the boundary only as
+``data_ptr()`` integers plus the current CUDA stream handle.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .exceptions import NumericalFailureError
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libnmfb.so")
+
+NMFB_OK = 0
+NMFB_ERR_NUMERIC = 1
+NMFB_ERR_ARG = 2
+NMFB_ERR_CUDA = 3
+NMFB_ERR_DEGENERATE = 4
+F32, F64 = 0, 1
+MODE_FAST, MODE_REFERENCE = 0, 1
+FAIL_NONE = -1
+FASTBREAK_BLOCK = 32
+UINT64_MAX = (1 << 64) - 1
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_f64 = ctypes.c_double
+_sz = ctypes.c_size_t
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+_pf64 = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes); mirrors include/nmfb.h
+SIGNATURES = {
+    "nmfb_version": (_int, []),
+    "nmfb_last_error": (ctypes.c_char_p, []),
+    "nmfb_device_sm_count": (_int, []),
+    "nmfb_estep_dense": (_int, [_int, _int, _vp, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _vp,
+                                _i32, _vp, _f64, _f64, _i32, _f64, _vp, _vp, _vp, _pi64, _pf64,
+                                _pi64, _vp]),
+    "nmfb_estep_sparse": (_int, [_int, _int, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _i32,
+                                 _vp, _vp, _vp, _i32, _vp, _f64, _f64, _i32, _f64, _vp, _vp, _vp,
+                                 _pi64, _pf64, _pi64, _vp]),
+    "nmfb_mstep_rows": (_int, [_int, _int, _vp, _i64, _i64, _vp, _vp, _vp, _i32, _vp, _f64, _f64,
+                               _i32, _f64, _vp, _i32, _pi64, _pf64, _pi64, _vp]),
+    "nmfb_nnls_batch": (_int, [_int, _int, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _int, _i32,
+                               _i64, _i64, _f64, _vp, _i64, _i64, _f64, _i32, _f64, _vp, _vp, _vp,
+                               _i32, _vp]),
+    "nmfb_nqp_solve": (_int, [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _f64, _i32, _f64,
+                              _vp, _vp, _vp, _i32, _vp, _vp]),
+    "nmfb_gram_workspace_bytes": (_sz, [_i64, _i32]),
+    "nmfb_gram": (_int, [_int, _vp, _i64, _i32, _i64, _vp, _vp, _vp]),
+    "nmfb_rescale": (_int, [_int, _vp, _i32, _f64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "nmfb_gemm_tall": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _i32, _i64, _vp, _i32, _vp]),
+    "nmfb_dense_linear_ref": (_int, [_int, _vp, _i64, _i64, _i64, _vp, _i32, _f64, _vp, _vp]),
+    "nmfb_dense_yt_ref": (_int, [_int, _vp, _i64, _i64, _vp, _i32, _pi64, _i32, _vp, _vp]),
+    "nmfb_hp_ref": (_int, [_int, _vp, _i64, _i32, _pi64, _i32, _vp, _vp]),
+    "nmfb_csc_linear": (_int, [_int, _int, _vp, _vp, _vp, _i64, _i64, _vp, _i32, _f64, _vp, _vp]),
+    "nmfb_csr_yt": (_int, [_int, _int, _vp, _vp, _vp, _i64, _vp, _i32, _int, _pi64, _i32, _vp,
+                           _vp]),
+    "nmfb_residual_workspace_bytes": (_sz, [_i64, _i64]),
+    "nmfb_dense_residual": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "nmfb_dot_workspace_bytes": (_sz, [_i64]),
+    "nmfb_dot": (_int, [_vp, _int, _vp, _int, _i64, _vp, _vp, _vp]),
+}
+
+_lib = None
+
+
+class NativeLibraryError(RuntimeError):
+    """libnmfb.so is missing or a CUDA call failed (no CPU fallback exists)."""
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryError(
+                f"{LIB_PATH} not found: build it with `python -m paper_1506_08938_b200.build` "
+                "(this package has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)
+
+
+def check(status, what):
+    if status == NMFB_OK:
+        return
+    if status == NMFB_ERR_CUDA:
+        msg = lib().nmfb_last_error().decode(errors="replace")
+        raise NativeLibraryError(f"{what}: CUDA error: {msg}")
+    if status == NMFB_ERR_ARG:
+        raise ValueError(f"{what}: invalid argument")
+    raise NativeLibraryError(f"{what}: status {status}")
+
+
+def call(name, *args):
+    status = getattr(lib(), name)(*args)
+    check(status, name)
+    return status
+
+
+def bounds_array(bounds):
+    arr = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    return arr, arr.ctypes.data_as(_pi64)
+
+
+def numeric_failure(what, index):
+    return NumericalFailureError(f"{what} failed at {index}", index=int(index))

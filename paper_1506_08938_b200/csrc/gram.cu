@@ -1,0 +1,216 @@
+// Gram products A^T A (G^T G for the coefficient step, F F^T for the
+// component step; matrix.py:181-197, kernels.py:276-280) and the fused
+// anti-lopsided rescale epilogue (nqp.py:116-131, parallel.py:87-91,104,196).
+//
+// Gram: CTA = 64x64 output tile x one row chunk; 256 threads each own a 4x4
+// register block; rows are staged 32 at a time in shared memory.  fp32 inputs
+// accumulate each 32-row slab in fp32 and fold it into fp64 accumulators
+// (products of fp32 values are exact in fp64 anyway); fp64 inputs accumulate
+// in fp64.  Chunk partials are summed in chunk order by a second kernel, so
+// the result is deterministic.  HBM roofline: reads rows*r*sizeof(T) once.
+#include <cmath>
+
+#include "common.cuh"
+#include "nmfb_internal.h"
+
+namespace nmfb {
+
+constexpr int GT = 64;      // output tile
+constexpr int GROWS = 32;   // rows per smem slab
+
+template <typename T>
+__global__ void __launch_bounds__(256) gram_partial_kernel(const T *__restrict__ A, int64_t rows,
+                                                           int r, int64_t lda, int64_t chunk,
+                                                           double *__restrict__ part) {
+    // blockIdx.x: tile pair (ti <= tj) index, blockIdx.y: row chunk
+    const int ntile = (r + GT - 1) / GT;
+    int t = blockIdx.x, ti = 0;
+    while (t >= ntile - ti) {
+        t -= ntile - ti;
+        ++ti;
+    }
+    const int tj = ti + t;
+    const int64_t row0 = (int64_t)blockIdx.y * chunk;
+    const int64_t row1 = min(rows, row0 + chunk);
+    __shared__ T Ai[GROWS][GT];
+    __shared__ T Aj[GROWS][GT];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+
+    for (int64_t rb = row0; rb < row1; rb += GROWS) {
+        for (int idx = threadIdx.x; idx < GROWS * GT; idx += 256) {
+            int rr = idx / GT, c = idx % GT;
+            int64_t row = rb + rr;
+            int ci = ti * GT + c, cj = tj * GT + c;
+            bool okr = row < row1;
+            Ai[rr][c] = (okr && ci < r) ? A[row * lda + ci] : T(0);
+            Aj[rr][c] = (okr && cj < r) ? A[row * lda + cj] : T(0);
+        }
+        __syncthreads();
+        T s[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) s[u][v] = T(0);
+#pragma unroll 8
+        for (int rr = 0; rr < GROWS; ++rr) {
+            T a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = Ai[rr][ty * 4 + u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) b[v] = Aj[rr][tx * 4 + v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) s[u][v] = fma(a[u], b[v], s[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] += (double)s[u][v];
+        __syncthreads();
+    }
+    double *out = part + (int64_t)blockIdx.y * r * r;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        int a = ti * GT + ty * 4 + u;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            int b = tj * GT + tx * 4 + v;
+            if (a < r && b < r && a <= b) out[a * r + b] = acc[u][v];
+        }
+    }
+}
+
+// out[a][b] = out[b][a] = sum_c part[c][min(a,b)][max(a,b)] in chunk order.
+__global__ void gram_reduce_kernel(const double *__restrict__ part, int nchunk, int r,
+                                   double *__restrict__ out) {
+    int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= r * r) return;
+    int a = idx / r, b = idx % r;
+    int lo = min(a, b), hi = max(a, b);
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += part[(int64_t)c * r * r + lo * r + hi];
+    out[idx] = s;
+}
+
+static int64_t gram_chunk(int64_t rows) {
+    // ~2 waves of 148 SMs worth of chunks, each a multiple of the slab height
+    int64_t target = 296;
+    int64_t chunk = (rows + target - 1) / target;
+    chunk = ((chunk + GROWS - 1) / GROWS) * GROWS;
+    if (chunk < 256) chunk = 256;
+    return chunk;
+}
+
+size_t gram_workspace_bytes(int64_t rows, int r) {
+    int64_t chunk = gram_chunk(rows);
+    int64_t nchunk = rows > 0 ? (rows + chunk - 1) / chunk : 1;
+    return (size_t)nchunk * r * r * sizeof(double);
+}
+
+int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, double *out,
+                void *ws, cudaStream_t st) {
+    if (r <= 0 || rows < 0) return NMFB_ERR_ARG;
+    int64_t chunk = gram_chunk(rows);
+    int64_t nchunk = rows > 0 ? (rows + chunk - 1) / chunk : 1;
+    double *part = (double *)ws;
+    int ntile = (r + GT - 1) / GT;
+    dim3 grid(ntile * (ntile + 1) / 2, (unsigned)nchunk);
+    if (rows == 0) {
+        cudaMemsetAsync(part, 0, sizeof(double) * r * r, st);
+    } else if (dtype == NMFB_F64) {
+        gram_partial_kernel<double><<<grid, 256, 0, st>>>((const double *)A, rows, r, lda, chunk,
+                                                          part);
+    } else {
+        gram_partial_kernel<float><<<grid, 256, 0, st>>>((const float *)A, rows, r, lda, chunk,
+                                                         part);
+    }
+    gram_reduce_kernel<<<(r * r + 255) / 256, 256, 0, st>>>(part, (int)nchunk, r, out);
+    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Rescale (single CTA): bit-exact restatement of nqp.rescale_arrays on
+// H = G + diag_add * I, compacted to the active dims (parallel.py:87-91).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) rescale_kernel(const double *__restrict__ G, int r,
+                                                      double diag_add, T *Qa, T *scale_a,
+                                                      int32_t *act_idx, uint8_t *active,
+                                                      int32_t *ra_dev, double *full_scale) {
+    extern __shared__ double sh[];
+    double *diag = sh;                         // r
+    int *pos = (int *)(sh + r);                // r: compact position or -1
+    __shared__ double s_delta;
+    __shared__ int s_ra;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < r; i += blockDim.x) {
+        // H = Q_g + (2.0 * mu2) * np.eye(r): the identity term adds diag_add * 1.0
+        diag[i] = __dadd_rn(G[i * r + i], __dmul_rn(diag_add, 1.0));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // np.max over the diagonal (NaN propagates)
+        double mx = diag[0];
+        bool nan = false;
+        for (int i = 0; i < r; ++i) {
+            if (isnan(diag[i])) nan = true;
+            if (diag[i] > mx) mx = diag[i];
+        }
+        if (nan) mx = __longlong_as_double(0x7ff8000000000000ULL);
+        s_delta = __dmul_rn(1e-12, mx);
+        int k = 0;
+        for (int i = 0; i < r; ++i) {
+            bool act = diag[i] > s_delta;
+            active[i] = act ? 1 : 0;
+            pos[i] = act ? k : -1;
+            if (act) act_idx[k++] = i;
+        }
+        s_ra = k;
+        *ra_dev = k;
+    }
+    __syncthreads();
+    const int ra = s_ra;
+    for (int i = tid; i < r; i += blockDim.x) {
+        double sc = __dsqrt_rn(diag[i]);
+        if (full_scale) full_scale[i] = sc;
+        if (pos[i] >= 0) scale_a[pos[i]] = (T)sc;
+    }
+    for (int idx = tid; idx < r * r; idx += blockDim.x) {
+        int i = idx / r, j = idx % r;
+        int pi = pos[i], pj = pos[j];
+        if (pi < 0 || pj < 0) continue;
+        double v;
+        if (i == j) {
+            v = 1.0;
+        } else {
+            double si = __dsqrt_rn(diag[i]), sj = __dsqrt_rn(diag[j]);
+            // off-diagonal of H = G + diag_add * eye: G_ij + 0.0
+            v = __ddiv_rn(__dadd_rn(G[i * r + j], 0.0), __dmul_rn(si, sj));
+        }
+        Qa[pi * ra + pj] = (T)v;
+    }
+}
+
+int rescale_launch(int dtype, const double *G, int r, double diag_add, void *Qa, void *scale_a,
+                   int32_t *act_idx, uint8_t *active, int32_t *ra_dev, double *full_scale,
+                   cudaStream_t st) {
+    if (r <= 0 || r > 4096) return NMFB_ERR_ARG;
+    size_t smem = r * sizeof(double) + r * sizeof(int);
+    if (dtype == NMFB_F64)
+        rescale_kernel<double><<<1, 256, smem, st>>>(G, r, diag_add, (double *)Qa,
+                                                     (double *)scale_a, act_idx, active, ra_dev,
+                                                     full_scale);
+    else
+        rescale_kernel<float><<<1, 256, smem, st>>>(G, r, diag_add, (float *)Qa,
+                                                    (float *)scale_a, act_idx, active, ra_dev,
+                                                    full_scale);
+    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+}
+
+}  // namespace nmfb

@@ -1,0 +1,41 @@
+// Internal launch descriptors shared by the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/nmfb.h"
+
+namespace nmfb {
+
+struct NnlsLaunch {
+    int dtype;         // NMFB_F32 | NMFB_F64 (type of Qa, scale_a, x, final_out)
+    int mode;          // NMFB_MODE_FAST | NMFB_MODE_REFERENCE
+    const void *Qa;    // (ra, ra) compact, row-major
+    const void *scale_a;
+    const int32_t *act_idx;
+    const uint8_t *active;
+    int r, ra;
+    const int32_t *ra_dev;  // nullable: device copy of ra (overrides ra)
+    const void *h;
+    int h_dtype;
+    int h_parts;
+    int64_t h_ld, h_pstride;
+    double h_base;
+    void *x;
+    int64_t count, index_base;
+    double eps;
+    int max_inner;
+    double max_stop0;
+    int32_t *iters_out;
+    void *final_out;
+    unsigned long long *stats;
+    void *hist = nullptr;  // reference kernel: (count, hist_ld, 2) norm/objective history
+    int hist_ld = 0;
+    bool independent = false;
+    int lanes;  // 0 = auto
+    cudaStream_t stream;
+};
+
+int nnls_launch(const NnlsLaunch &p);
+
+}  // namespace nmfb

@@ -1,0 +1,251 @@
+// Sparse data products for CSC/CSR data (kernels.py:251-258 linear terms,
+// kernels.py:270-274 Y^T accumulator).  Warp per data column (CSC) or row
+// (CSR); lanes own components i = lane + 32c, so every G / F^T row gather is
+// one coalesced r-float read.  Nonzeros are fetched 32 at a time by the lanes
+// and broadcast by shuffles.  Each output is a sequential sum over the
+// column's / row's nonzeros in storage order: in NMFB_MODE_REFERENCE with
+// unfused arithmetic that is exactly the reference's order (bit-exact fp64).
+// HBM roofline per pass: nnz*(4 + sizeof(T)) + (m or n + 1)*8 bytes of index
+// data + the gathered rows (L2-resident at C3).
+#include "common.cuh"
+#include "nmfb_internal.h"
+
+namespace nmfb {
+
+template <typename T, bool EXACT, int C>
+__global__ void __launch_bounds__(128) csc_linear_kernel(const int64_t *__restrict__ indptr,
+                                                         const int32_t *__restrict__ rowidx,
+                                                         const T *__restrict__ vals,
+                                                         int64_t col_lo, int64_t col_hi,
+                                                         const T *__restrict__ G, int r, T mu1,
+                                                         T *__restrict__ h) {
+    const int64_t col = col_lo + (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (col >= col_hi) return;
+    const int lane = threadIdx.x & 31;
+    T acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = mu1;
+    const int64_t p0 = indptr[col], p1 = indptr[col + 1];
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int myrow = 0;
+        T myv = T(0);
+        if (lane < cnt) {
+            myrow = rowidx[base + lane];
+            myv = vals[base + lane];
+        }
+        for (int u = 0; u < cnt; ++u) {
+            const int row = __shfl_sync(NMFB_FULL_MASK, myrow, u);
+            const T v = __shfl_sync(NMFB_FULL_MASK, myv, u);
+            const T *grow = G + (int64_t)row * r;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int i = lane + 32 * c;
+                if (i < r) {
+                    if (EXACT)
+                        acc[c] = Exact<T>::msub(acc[c], grow[i], v);
+                    else
+                        acc[c] = fma(-grow[i], v, acc[c]);
+                }
+            }
+        }
+    }
+    T *out = h + (col - col_lo) * r;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int i = lane + 32 * c;
+        if (i < r) out[i] = acc[c];
+    }
+}
+
+struct SparseShards {
+    int64_t b[NMFB_MAX_WORKERS + 1];
+    int w;
+};
+
+// YT[row][i] = sum over the row's entries (ascending column) FT[col][i] * v.
+// With shards: per-worker partial sums, added in worker order (the reference
+// reduce, parallel.py:150-156).
+template <typename T, typename TY, bool EXACT, int C>
+__global__ void __launch_bounds__(128) csr_yt_kernel(const int64_t *__restrict__ rowptr,
+                                                     const int32_t *__restrict__ colidx,
+                                                     const T *__restrict__ vals, int64_t n,
+                                                     const T *__restrict__ FT, int r,
+                                                     SparseShards sh, TY *__restrict__ YT) {
+    const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    const int lane = threadIdx.x & 31;
+    TY total[C], acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) total[c] = acc[c] = TY(0);
+    int w = 0;
+    int64_t whi = sh.b[1];
+    const int64_t p0 = rowptr[row], p1 = rowptr[row + 1];
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int mycol = 0;
+        T myv = T(0);
+        if (lane < cnt) {
+            mycol = colidx[base + lane];
+            myv = vals[base + lane];
+        }
+        for (int u = 0; u < cnt; ++u) {
+            const int col = __shfl_sync(NMFB_FULL_MASK, mycol, u);
+            const T v = __shfl_sync(NMFB_FULL_MASK, myv, u);
+            if (EXACT) {
+                while (col >= whi && w + 1 < sh.w) {  // next worker shard
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        total[c] = Exact<TY>::add(total[c], acc[c]);
+                        acc[c] = TY(0);
+                    }
+                    ++w;
+                    whi = sh.b[w + 1];
+                }
+            }
+            const T *f = FT + (int64_t)col * r;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int i = lane + 32 * c;
+                if (i < r) {
+                    if (EXACT)
+                        acc[c] = Exact<TY>::madd(acc[c], (TY)f[i], (TY)v);
+                    else
+                        acc[c] = fma((TY)f[i], (TY)v, acc[c]);
+                }
+            }
+        }
+    }
+    TY *out = YT + row * r;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int i = lane + 32 * c;
+        if (i < r) out[i] = EXACT ? Exact<TY>::add(total[c], acc[c]) : acc[c];
+    }
+}
+
+template <typename T, bool EXACT>
+static int csc_linear_dispatch(const int64_t *indptr, const int32_t *rowidx, const void *vals,
+                               int64_t lo, int64_t hi, const void *G, int r, double mu1, void *h,
+                               cudaStream_t st) {
+    dim3 grid((unsigned)((hi - lo + 3) / 4));
+    const T *v = (const T *)vals;
+    const T *g = (const T *)G;
+    T *o = (T *)h;
+#define NMFB_CSC(Cc) \
+    csc_linear_kernel<T, EXACT, Cc><<<grid, 128, 0, st>>>(indptr, rowidx, v, lo, hi, g, r, (T)mu1, o)
+    if (r <= 32)
+        NMFB_CSC(1);
+    else if (r <= 64)
+        NMFB_CSC(2);
+    else if (r <= 128)
+        NMFB_CSC(4);
+    else if (r <= 256)
+        NMFB_CSC(8);
+    else
+        return NMFB_ERR_ARG;
+#undef NMFB_CSC
+    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+}
+
+int csc_linear_launch(int dtype, int mode, const int64_t *indptr, const int32_t *rowidx,
+                      const void *vals, int64_t lo, int64_t hi, const void *G, int r, double mu1,
+                      void *h, cudaStream_t st) {
+    if (hi <= lo) return NMFB_OK;
+    bool exact = (mode == NMFB_MODE_REFERENCE);
+    if (dtype == NMFB_F64)
+        return exact ? csc_linear_dispatch<double, true>(indptr, rowidx, vals, lo, hi, G, r, mu1,
+                                                         h, st)
+                     : csc_linear_dispatch<double, false>(indptr, rowidx, vals, lo, hi, G, r,
+                                                          mu1, h, st);
+    return exact ? csc_linear_dispatch<float, true>(indptr, rowidx, vals, lo, hi, G, r, mu1, h, st)
+                 : csc_linear_dispatch<float, false>(indptr, rowidx, vals, lo, hi, G, r, mu1, h,
+                                                     st);
+}
+
+template <typename T, typename TY, bool EXACT>
+static int csr_yt_dispatch(const int64_t *rowptr, const int32_t *colidx, const void *vals,
+                           int64_t n, const void *FT, int r, const SparseShards &sh, void *YT,
+                           cudaStream_t st) {
+    dim3 grid((unsigned)((n + 3) / 4));
+    const T *v = (const T *)vals;
+    const T *f = (const T *)FT;
+    TY *o = (TY *)YT;
+#define NMFB_CSR(Cc) \
+    csr_yt_kernel<T, TY, EXACT, Cc><<<grid, 128, 0, st>>>(rowptr, colidx, v, n, f, r, sh, o)
+    if (r <= 32)
+        NMFB_CSR(1);
+    else if (r <= 64)
+        NMFB_CSR(2);
+    else if (r <= 128)
+        NMFB_CSR(4);
+    else if (r <= 256)
+        NMFB_CSR(8);
+    else
+        return NMFB_ERR_ARG;
+#undef NMFB_CSR
+    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+}
+
+int csr_yt_launch(int dtype, int mode, const int64_t *rowptr, const int32_t *colidx,
+                  const void *vals, int64_t n, const void *FT, int r, int yt_dtype,
+                  const int64_t *bounds, int workers, void *YT, cudaStream_t st) {
+    if (n <= 0) return NMFB_OK;
+    SparseShards sh;
+    if (workers < 1 || workers > NMFB_MAX_WORKERS) return NMFB_ERR_ARG;
+    sh.w = workers;
+    for (int i = 0; i <= workers; ++i) sh.b[i] = bounds ? bounds[i] : (i == 0 ? 0 : INT64_MAX);
+    bool exact = (mode == NMFB_MODE_REFERENCE);
+    if (dtype == NMFB_F64) {
+        if (yt_dtype != NMFB_F64) return NMFB_ERR_ARG;
+        return exact ? csr_yt_dispatch<double, double, true>(rowptr, colidx, vals, n, FT, r, sh,
+                                                             YT, st)
+                     : csr_yt_dispatch<double, double, false>(rowptr, colidx, vals, n, FT, r, sh,
+                                                              YT, st);
+    }
+    if (yt_dtype == NMFB_F64)
+        return exact ? csr_yt_dispatch<float, double, true>(rowptr, colidx, vals, n, FT, r, sh, YT,
+                                                            st)
+                     : csr_yt_dispatch<float, double, false>(rowptr, colidx, vals, n, FT, r, sh,
+                                                             YT, st);
+    return exact ? csr_yt_dispatch<float, float, true>(rowptr, colidx, vals, n, FT, r, sh, YT, st)
+                 : csr_yt_dispatch<float, float, false>(rowptr, colidx, vals, n, FT, r, sh, YT,
+                                                        st);
+}
+
+// Drop-in (nmfb_estep_sparse) accumulator: YT[row][i] += x[col][i] * v for the
+// shard's columns in column order -- one thread per component walks the
+// shard's nonzeros serially, which keeps the reference's per-entry order
+// (kernels.py:270-274).  Check/drop-in path only; fit() uses csr_yt_kernel.
+template <typename T>
+__global__ void csc_scatter_yt_kernel(const int64_t *__restrict__ indptr,
+                                      const int32_t *__restrict__ rowidx,
+                                      const T *__restrict__ vals, int64_t lo, int64_t hi,
+                                      const T *__restrict__ FT, int r, T *__restrict__ YT) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= r) return;
+    for (int64_t col = lo; col < hi; ++col) {
+        const T x = FT[col * r + i];
+        for (int64_t t = indptr[col]; t < indptr[col + 1]; ++t) {
+            T *dst = YT + (int64_t)rowidx[t] * r + i;
+            *dst = Exact<T>::madd(*dst, x, vals[t]);
+        }
+    }
+}
+
+int csc_scatter_yt_launch(int dtype, const int64_t *indptr, const int32_t *rowidx,
+                          const void *vals, int64_t lo, int64_t hi, const void *FT, int r,
+                          void *YT, cudaStream_t st) {
+    if (hi <= lo) return NMFB_OK;
+    dim3 grid((unsigned)((r + 63) / 64));
+    if (dtype == NMFB_F64)
+        csc_scatter_yt_kernel<double><<<grid, 64, 0, st>>>(indptr, rowidx, (const double *)vals,
+                                                          lo, hi, (const double *)FT, r,
+                                                          (double *)YT);
+    else
+        csc_scatter_yt_kernel<float><<<grid, 64, 0, st>>>(indptr, rowidx, (const float *)vals, lo,
+                                                         hi, (const float *)FT, r, (float *)YT);
+    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+}
+
+}  // namespace nmfb

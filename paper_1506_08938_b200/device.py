@@ -1,0 +1,428 @@
+"""Device-side state and the per-iteration launch sequence of the alternation.
+
+Torch is used for allocation, host<->device copies, streams and events only;
+every numeric step is a libnmfb.so kernel reached through the C ABI
+(include/nmfb.h).  The launch sequence of one outer iteration follows
+nmf.py:188-196 (gram -> coefficient step -> component step -> objective):
+
+  gram(G) -> rescale(+2 mu2)                      Q_g, compact Qa   (matrix.py:181, nqp.py:116)
+  linear terms h = mu1 - G^T X                    dense GEMM / CSC SpMM (kernels.py:251,306)
+  batched NNLS over the m columns -> F           nnls kernels (kernels.py:178-220)
+  H_f = F F^T ; Y^T = X F^T                       gram / dense GEMM / CSR SpMM (kernels.py:270-280)
+  rescale(H_f + 2 beta2) ; NNLS over n rows -> G  (parallel.py:189-223, kernels.py:339-378)
+  objective pieces                                residual (dense) / trace identity (sparse)
+
+Two precisions:
+  * "fp64": reference-order kernels (NMFB_MODE_REFERENCE) in float64; the
+    per-worker shard partial sums of the reference's reduce are emulated, so
+    run_estep / run_mstep are bit-identical to the reference given the same
+    inputs (only the BLAS Gram differs in the last bits).
+  * "fp32": production path -- split-K GEMM / SpMM passes and the register
+    resident warp-group NNLS kernel in float32, fp64 reductions.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .exceptions import NumericalFailureError
+from .matrix import DenseMatrix, SparseMatrix
+
+_TORCH = {"fp32": torch.float32, "fp64": torch.float64}
+_CODE = {"fp32": L.F32, "fp64": L.F64}
+
+
+def require_cuda():
+    L.lib()
+    if not torch.cuda.is_available():
+        raise L.NativeLibraryError("no CUDA device: libnmfb.so requires a B200 (sm_100a)")
+    return torch.device("cuda")
+
+
+def vp(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def plan(total, workers):
+    """parallel.py:72-84."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    workers = min(workers, total) if total > 0 else 1
+    base, extra = divmod(total, workers)
+    shards, lo = [], 0
+    for w in range(workers):
+        hi = lo + base + (1 if w < extra else 0)
+        shards.append((lo, hi))
+        lo = hi
+    return shards
+
+
+def block_plan(total, workers):
+    """parallel.py:162-169: shards aligned to FASTBREAK_BLOCK."""
+    b = L.FASTBREAK_BLOCK
+    nblocks = max(-(-total // b), 1)
+    return [(lo * b, min(hi * b, total)) for lo, hi in plan(nblocks, workers)]
+
+
+def shard_bounds(total, workers):
+    shards = block_plan(total, workers)
+    return [shards[0][0]] + [hi for _, hi in shards]
+
+
+# ---------------------------------------------------------------------------
+# data matrix on the device
+# ---------------------------------------------------------------------------
+class DeviceData:
+    """X on the device.  Dense: XT (m, n) row-major == the reference's
+    Fortran-ordered (n, m) buffer.  Sparse: CSC (int64 indptr, int32 rows,
+    values) plus the CSR of the same matrix (int64 rowptr, int32 cols
+    ascending per row)."""
+
+    def __init__(self, V, precision="fp32", device=None, stream=None):
+        self.device = device or require_cuda()
+        self.precision = precision
+        dt = _TORCH[precision]
+        if isinstance(V, DenseMatrix):
+            V = V.array
+        if isinstance(V, SparseMatrix):
+            self.kind = "sparse"
+            self.n, self.m = V.rows, V.cols
+            if V.nnz >= 2**31 or self.n >= 2**31 or self.m >= 2**31:
+                raise ValueError("sparse sizes must fit int32 indices")
+            rowptr, colidx, cvals = V.csr()
+            self.indptr = torch.from_numpy(V.indptr).to(self.device, non_blocking=True)
+            self.rowidx = torch.from_numpy(V.indices.astype(np.int32)).to(self.device)
+            self.vals = torch.from_numpy(V.values).to(self.device, dt)
+            self.rowptr = torch.from_numpy(rowptr).to(self.device)
+            self.colidx = torch.from_numpy(colidx.astype(np.int32)).to(self.device)
+            self.cvals = torch.from_numpy(cvals).to(self.device, dt)
+            self.xsq = V.sum_squares()
+            self.nnz = V.nnz
+            self.host = V
+        else:
+            arr = np.asarray(V)
+            if arr.ndim != 2:
+                raise ValueError("dense data must be 2-D")
+            self.kind = "dense"
+            self.n, self.m = arr.shape
+            xt = np.ascontiguousarray(arr.T)  # no copy for Fortran input
+            if dt == torch.float32 and xt.dtype != np.float32:
+                xt = xt.astype(np.float32)
+            elif dt == torch.float64 and xt.dtype != np.float64:
+                xt = xt.astype(np.float64)
+            self.XT = torch.from_numpy(xt).to(self.device)
+            self.host = None
+
+    @classmethod
+    def from_device_dense(cls, XT, precision):
+        """Wrap an existing (m, n) device tensor (already in HBM)."""
+        self = cls.__new__(cls)
+        self.device = XT.device
+        self.precision = precision
+        self.kind = "dense"
+        self.m, self.n = XT.shape
+        self.XT = XT
+        self.host = None
+        return self
+
+
+# ---------------------------------------------------------------------------
+# one alternation state on the device
+# ---------------------------------------------------------------------------
+class Alternation:
+    """Device state of fit(): G (n, r), FT (m, r) and all step buffers."""
+
+    def __init__(self, data: DeviceData, cfg, G0, FT0, max_iters, precision="fp32", lanes=0,
+                 kernel_mode=None, splits=None):
+        self.d = data
+        self.cfg = cfg
+        self.prec = precision
+        self.code = _CODE[precision]
+        self.mode = (L.MODE_REFERENCE if precision == "fp64" else L.MODE_FAST) \
+            if kernel_mode is None else kernel_mode
+        self.lanes = lanes
+        dev = data.device
+        dt = _TORCH[precision]
+        n, m, r = data.n, data.m, cfg.rank
+        self.n, self.m, self.r = n, m, r
+        f64 = torch.float64
+        self.G = torch.as_tensor(np.ascontiguousarray(G0), dtype=dt).to(dev)
+        self.FT = torch.as_tensor(np.ascontiguousarray(FT0), dtype=dt).to(dev)
+        self.Qg = torch.zeros((r, r), dtype=f64, device=dev)
+        self.Hf = torch.zeros((r, r), dtype=f64, device=dev)
+        # compact rescaled problems of the two steps
+        self.Qa = [torch.zeros((r * r,), dtype=dt, device=dev) for _ in range(2)]
+        self.sa = [torch.zeros((r,), dtype=dt, device=dev) for _ in range(2)]
+        self.act = [torch.zeros((r,), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.active = [torch.zeros((r,), dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.ra = [torch.zeros((1,), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.gram_ws = torch.empty((L.lib().nmfb_gram_workspace_bytes(max(n, m), r) // 8 + 1,),
+                                   dtype=f64, device=dev)
+        self.dot_ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=f64,
+                                  device=dev)
+        sms = max(L.lib().nmfb_device_sm_count(), 1)
+        if data.kind == "dense":
+            self.res_ws = torch.empty((L.lib().nmfb_residual_workspace_bytes(m, n) // 8 + 1,),
+                                      dtype=f64, device=dev)
+        if data.kind == "dense" and self.mode == L.MODE_FAST:
+            # split-K factors: ~4 CTAs per SM for each pass
+            self.splits_e = splits or self._splits(m, n, sms)
+            self.splits_m = splits or self._splits(n, m, sms)
+            self.hbuf = torch.empty((self.splits_e * m * r,), dtype=torch.float32, device=dev)
+            self.ybuf = torch.empty((self.splits_m * n * r,), dtype=torch.float32, device=dev)
+        else:
+            self.hbuf = torch.empty((m * r,), dtype=dt, device=dev)
+            ydt = f64 if (data.kind == "sparse" or precision == "fp64") else dt
+            self.ybuf = torch.empty((n * r,), dtype=ydt, device=dev)
+        self.max_iters = max_iters
+        # per iteration: stats [2 steps][inner, fail], objective pieces
+        self.stats = torch.zeros((max_iters, 2, 2), dtype=torch.int64, device=dev)
+        self.stats[:, :, 1] = -1  # == UINT64_MAX
+        self.pieces = torch.zeros((max_iters, 12), dtype=f64, device=dev)
+        if precision == "fp64" or data.kind == "sparse":
+            self.bounds_e = shard_bounds(m, cfg.workers)
+        else:
+            self.bounds_e = [0, m]
+        self.qg_valid = False
+
+    @staticmethod
+    def _splits(M, K, sms):
+        tiles = -(-M // 128)
+        s = max(1, round(4 * sms / tiles))
+        s = min(s, max(1, K // 256))
+        return int(s)
+
+    # -- primitive launches ------------------------------------------------
+    def _st(self):
+        return stream_handle()
+
+    def gram(self, A, rows, out):
+        L.call("nmfb_gram", self.code, vp(A), rows, self.r, self.r, vp(out), vp(self.gram_ws),
+               self._st())
+
+    def rescale(self, H, diag_add, side):
+        L.call("nmfb_rescale", self.code, vp(H), self.r, diag_add, vp(self.Qa[side]),
+               vp(self.sa[side]), vp(self.act[side]), vp(self.active[side]), vp(self.ra[side]),
+               None, self._st())
+
+    def nnls(self, side, h, h_dtype, parts, h_ld, pstride, h_base, x, count, stats):
+        L.call("nmfb_nnls_batch", self.code, self.mode, vp(self.Qa[side]), vp(self.sa[side]),
+               vp(self.act[side]), vp(self.active[side]), self.r, self.r, vp(self.ra[side]),
+               vp(h), h_dtype, parts, h_ld, pstride, h_base, vp(x), count, 0,
+               float(self.cfg.epsilon), int(self.cfg.inner_cap), 0.0, None, None, vp(stats),
+               self.lanes, self._st())
+
+    def dot(self, a, a_code, b, b_code, length, out):
+        L.call("nmfb_dot", vp(a), a_code, vp(b), b_code, length, vp(out), vp(self.dot_ws),
+               self._st())
+
+    # -- the two half-steps ---------------------------------------------------
+    def estep(self, k):
+        """Coefficient step (parallel.run_estep): linear terms, NNLS over the
+        m columns, then the accumulators H_f = F F^T and Y^T = X F^T."""
+        cfg, d, r = self.cfg, self.d, self.r
+        n, m = self.n, self.m
+        if not self.qg_valid:
+            self.gram(self.G, n, self.Qg)
+        self.qg_valid = False
+        self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
+        st = self.stats[k, 0]
+        if d.kind == "dense":
+            if self.mode == L.MODE_FAST:
+                L.call("nmfb_gemm_tall", vp(d.XT), 1, m, n, n, vp(self.G), r, r, vp(self.hbuf),
+                       self.splits_e, self._st())
+                self.nnls(0, self.hbuf, L.F32, self.splits_e, r, m * r, cfg.mu1, self.FT, m, st)
+            else:
+                L.call("nmfb_dense_linear_ref", self.code, vp(d.XT), n, 0, m, vp(self.G), r,
+                       cfg.mu1, vp(self.hbuf), self._st())
+                self.nnls(0, self.hbuf, self.code, 0, r, 0, 0.0, self.FT, m, st)
+        else:
+            L.call("nmfb_csc_linear", self.code, self.mode, vp(d.indptr), vp(d.rowidx),
+                   vp(d.vals), 0, m, vp(self.G), r, cfg.mu1, vp(self.hbuf), self._st())
+            self.nnls(0, self.hbuf, self.code, 0, r, 0, 0.0, self.FT, m, st)
+        # accumulators from the new coefficients
+        ba, bp = L.bounds_array(self.bounds_e)
+        W = len(self.bounds_e) - 1
+        if self.prec == "fp64" or self.mode == L.MODE_REFERENCE:
+            L.call("nmfb_hp_ref", self.code, vp(self.FT), m, r, bp, W, vp(self.Hf), self._st())
+        else:
+            self.gram(self.FT, m, self.Hf)
+        if d.kind == "dense":
+            if self.mode == L.MODE_FAST:
+                L.call("nmfb_gemm_tall", vp(d.XT), 0, n, m, n, vp(self.FT), r, r,
+                       vp(self.ybuf), self.splits_m, self._st())
+            else:
+                L.call("nmfb_dense_yt_ref", self.code, vp(d.XT), m, n, vp(self.FT), r, bp, W,
+                       vp(self.ybuf), self._st())
+        else:
+            ycode = L.F64 if self.ybuf.dtype == torch.float64 else L.F32
+            L.call("nmfb_csr_yt", self.code, self.mode, vp(d.rowptr), vp(d.colidx), vp(d.cvals),
+                   n, vp(self.FT), r, ycode, bp, W, vp(self.ybuf), self._st())
+        del ba
+
+    def mstep(self, k):
+        """Component step (parallel.run_mstep): NNLS over the n rows with
+        h = beta1 - Y^T."""
+        cfg = self.cfg
+        self.rescale(self.Hf, 2.0 * cfg.beta2, 1)
+        st = self.stats[k, 1]
+        if self.d.kind == "dense" and self.mode == L.MODE_FAST:
+            self.nnls(1, self.ybuf, L.F32, self.splits_m, self.r, self.n * self.r, cfg.beta1,
+                      self.G, self.n, st)
+        else:
+            ycode = L.F64 if self.ybuf.dtype == torch.float64 else L.F32
+            self.nnls(1, self.ybuf, ycode, 1, self.r, 0, cfg.beta1, self.G, self.n, st)
+
+    def objective(self, k):
+        """Objective pieces of iteration k into self.pieces[k] (nmf.py:152-165)."""
+        cfg, d = self.cfg, self.d
+        p = self.pieces[k]
+        if d.kind == "dense":
+            # 0.5 ||X - G F||^2 by tile residual; G F never stored
+            L.call("nmfb_dense_residual", self.code, vp(d.XT), self.m, self.n, vp(self.G),
+                   vp(self.FT), self.r, vp(p[0:1]), vp(self.res_ws), self._st())
+        else:
+            # trace identity (matrix.py:240-253): cross = <G, Y^T>, quad = <G^T G, F F^T>
+            self.dot(self.G, self.code, self.ybuf, L.F64, self.n * self.r, p[1:4])
+            self.gram(self.G, self.n, self.Qg)
+            self.qg_valid = True  # reused by the next coefficient step
+            self.dot(self.Qg, L.F64, self.Hf, L.F64, self.r * self.r, p[7:10])
+        # penalty sums: slots 4..6 = (-, sum|F|, sum F^2); 1..3 = (cross, sum|G|, sum G^2)
+        if cfg.mu1 or cfg.mu2:
+            self.dot(self.FT, self.code, None, L.F64, self.m * self.r, p[4:7])
+        if (cfg.beta1 or cfg.beta2) and d.kind == "dense":
+            self.dot(self.G, self.code, None, L.F64, self.n * self.r, p[1:4])
+
+    def iterate(self, k):
+        self.estep(k)
+        self.mstep(k)
+        self.objective(k)
+
+    # -- host views ------------------------------------------------------------
+    @staticmethod
+    def assemble(pieces, cfg, kind, xsq):
+        """nmf.py:152-165 from the device pieces (host fp64 scalar algebra)."""
+        if kind == "dense":
+            value = pieces[0]
+        else:
+            value = 0.5 * (xsq - 2.0 * pieces[1] + pieces[7])
+        if cfg.mu1:
+            value += cfg.mu1 * pieces[5]
+        if cfg.beta1:
+            value += cfg.beta1 * pieces[2]
+        if cfg.mu2:
+            value += cfg.mu2 * pieces[6]
+        if cfg.beta2:
+            value += cfg.beta2 * pieces[3]
+        return float(value)
+
+    def failure(self, stats_host, k):
+        """First failing (step, index) at iteration k, or None."""
+        for step, what in ((0, "coefficient solve failed at column"),
+                           (1, "component solve failed at row")):
+            f = int(stats_host[k, step, 1])
+            if f != -1:
+                return NumericalFailureError(f"{what} {f}", index=f)
+        return None
+
+    def factors_host(self):
+        return (self.G.double().cpu().numpy(), self.FT.double().cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# small host-API helpers (gram / objective of host arrays, on the device)
+# ---------------------------------------------------------------------------
+def gram_host(arr):
+    dev = require_cuda()
+    a = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(dev)
+    rows, r = a.shape
+    out = torch.empty((r, r), dtype=torch.float64, device=dev)
+    ws = torch.empty((L.lib().nmfb_gram_workspace_bytes(rows, r) // 8 + 1,), dtype=torch.float64,
+                     device=dev)
+    L.call("nmfb_gram", L.F64, vp(a), rows, r, r, vp(out), vp(ws), stream_handle())
+    return out.cpu().numpy()
+
+
+def sparse_col_times_dense_host(v, col, g_arr):
+    dev = require_cuda()
+    g = torch.from_numpy(np.ascontiguousarray(g_arr, dtype=np.float64)).to(dev)
+    lo, hi = int(v.indptr[col]), int(v.indptr[col + 1])
+    r = g.shape[1]
+    indptr = torch.tensor([0, hi - lo], dtype=torch.int64, device=dev)
+    rows = torch.from_numpy(v.indices[lo:hi].astype(np.int32)).to(dev)
+    vals = torch.from_numpy(v.values[lo:hi]).to(dev)
+    h = torch.empty((r,), dtype=torch.float64, device=dev)
+    L.call("nmfb_csc_linear", L.F64, L.MODE_REFERENCE, vp(indptr), vp(rows) if hi > lo else None,
+           vp(vals) if hi > lo else None, 0, 1, vp(g), r, 0.0, vp(h), stream_handle())
+    return -h.cpu().numpy()
+
+
+def frobenius_objective_host(v, g_arr, f_arr):
+    dev = require_cuda()
+    r = g_arr.shape[1]
+    G = torch.from_numpy(np.ascontiguousarray(g_arr, dtype=np.float64)).to(dev)
+    FT = torch.from_numpy(np.ascontiguousarray(f_arr.T, dtype=np.float64)).to(dev)
+    out = torch.zeros((12,), dtype=torch.float64, device=dev)
+    if isinstance(v, SparseMatrix):
+        d = DeviceData(v, "fp64", dev)
+        Y = torch.empty((d.n, r), dtype=torch.float64, device=dev)
+        ba, bp = L.bounds_array([0, d.m])
+        L.call("nmfb_csr_yt", L.F64, L.MODE_FAST, vp(d.rowptr), vp(d.colidx), vp(d.cvals), d.n,
+               vp(FT), r, L.F64, bp, 1, vp(Y), stream_handle())
+        ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=torch.float64,
+                         device=dev)
+        L.call("nmfb_dot", vp(G), L.F64, vp(Y), L.F64, d.n * r, vp(out[1:4]), vp(ws),
+               stream_handle())
+        Hf = torch.empty((r, r), dtype=torch.float64, device=dev)
+        Qg = torch.empty((r, r), dtype=torch.float64, device=dev)
+        gws = torch.empty((L.lib().nmfb_gram_workspace_bytes(max(d.n, d.m), r) // 8 + 1,),
+                          dtype=torch.float64, device=dev)
+        L.call("nmfb_gram", L.F64, vp(FT), d.m, r, r, vp(Hf), vp(gws), stream_handle())
+        L.call("nmfb_gram", L.F64, vp(G), d.n, r, r, vp(Qg), vp(gws), stream_handle())
+        L.call("nmfb_dot", vp(Qg), L.F64, vp(Hf), L.F64, r * r, vp(out[7:10]), vp(ws),
+               stream_handle())
+        p = out.cpu().numpy()
+        return 0.5 * (v.sum_squares() - 2.0 * p[1] + p[7])
+    arr = v.array if isinstance(v, DenseMatrix) else np.asarray(v, dtype=np.float64)
+    d = DeviceData(arr, "fp64", dev)
+    ws = torch.empty((L.lib().nmfb_residual_workspace_bytes(d.m, d.n) // 8 + 1,),
+                     dtype=torch.float64, device=dev)
+    L.call("nmfb_dense_residual", L.F64, vp(d.XT), d.m, d.n, vp(G), vp(FT), r, vp(out[0:1]),
+           vp(ws), stream_handle())
+    return float(out[0].item())
+
+
+def matvec_t_host(g_arr, v):
+    """G^T v for a dense column (nmf.build_estep_problem), reference order."""
+    dev = require_cuda()
+    g = torch.from_numpy(np.ascontiguousarray(g_arr, dtype=np.float64)).to(dev)
+    vt = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)[None, :]).to(dev)
+    n, r = g.shape
+    h = torch.empty((r,), dtype=torch.float64, device=dev)
+    L.call("nmfb_dense_linear_ref", L.F64, vp(vt), n, 0, 1, vp(g), r, 0.0, vp(h),
+           stream_handle())
+    return -h.cpu().numpy()
+
+
+def abs_sq_sums_host(arrays):
+    """[(sum |a|, sum a^2) for each array] with fp64 device reductions."""
+    dev = require_cuda()
+    ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=torch.float64,
+                     device=dev)
+    out = []
+    for a in arrays:
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+        o = torch.zeros((3,), dtype=torch.float64, device=dev)
+        L.call("nmfb_dot", vp(t), L.F64, None, L.F64, t.numel(), vp(o), vp(ws), stream_handle())
+        oo = o.cpu().numpy()
+        out.append((float(oo[1]), float(oo[2])))
+    return out

@@ -1,0 +1,263 @@
+"""Alternating factorization driver on the B200 (reference nmf.py API).
+
+``fit(V, cfg, on_iteration=None)`` runs the reference's alternation
+(nmf.py:168-211) with every numeric step on the GPU (device.Alternation).
+The reference's ``fit`` reads an undefined global ``on_iteration``
+(nmf.py:197); here it is the evident intended keyword: a
+callback invoked with the ConvergenceLog after every outer iteration.
+
+Host work per fit: seeded factor initialisation (numpy PCG64, exactly
+nmf.py:115-127 so both sides start from identical bits), one upload of X and
+the factors, one download of the factors and the per-iteration log.  Without
+an early-exit tolerance or a callback there is no host synchronisation
+inside the loop.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as D
+from .exceptions import NumericalFailureError
+from .matrix import (DenseMatrix, SparseMatrix, frobenius_objective, require_nonnegative,
+                     sparse_col_times_dense)
+from .nqp import DEFAULT_EPSILON, DEFAULT_MAX_INNER, NqpProblem
+
+PRECISIONS = ("fp32", "fp64")
+
+
+@dataclass
+class NmfConfig:
+    """Knobs for one factorization run (nmf.py:34-70).
+
+    B200 additions: ``precision`` -- "fp32" (production kernels) or "fp64"
+    (reference-order check mode, bit-exact steps); ``lanes`` -- lanes per
+    subproblem of the fp32 NNLS kernel (0 = auto).
+    """
+
+    rank: int
+    max_outer: int = 300
+    epsilon: float = DEFAULT_EPSILON
+    mu1: float = 0.0
+    mu2: float = 0.0
+    beta1: float = 0.0
+    beta2: float = 0.0
+    workers: int = 1
+    seed: int = 0
+    inner_cap: int = DEFAULT_MAX_INNER
+    rel_change_tol: float = 1e-10
+    precision: str = "fp32"
+    lanes: int = 0
+
+    def __post_init__(self):
+        if self.rank < 1:
+            raise ValueError("rank must be >= 1")
+        if not 0.0 <= self.epsilon <= 1.0:
+            raise ValueError("epsilon must lie in [0, 1]")
+        for name in ("mu1", "mu2", "beta1", "beta2"):
+            if getattr(self, name) < 0.0:
+                raise ValueError(f"{name} must be >= 0")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.max_outer < 1:
+            raise ValueError("max_outer must be >= 1")
+        if self.inner_cap < 1:
+            raise ValueError("inner_cap must be >= 1")
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {PRECISIONS}")
+        if self.rank > 256:
+            raise ValueError("rank must be <= 256 on this build")
+
+
+@dataclass
+class NmfModel:
+    """Nonnegative factors: components G (n x r) and coefficients F (r x m)."""
+
+    G: DenseMatrix
+    F: DenseMatrix
+
+
+@dataclass
+class ConvergenceLog:
+    """nmf.py:81-102: objective, cumulative seconds, inner iterations, k_bar."""
+
+    objective: list = field(default_factory=list)
+    seconds: list = field(default_factory=list)
+    inner_iterations: list = field(default_factory=list)
+    k_bar: list = field(default_factory=list)
+
+    def append(self, objective, seconds, inner_iterations, subproblems):
+        self.objective.append(float(objective))
+        self.seconds.append(float(seconds))
+        self.inner_iterations.append(int(inner_iterations))
+        self.k_bar.append(inner_iterations / subproblems)
+
+    def __len__(self):
+        return len(self.objective)
+
+    @property
+    def final_objective(self):
+        return self.objective[-1]
+
+
+def _shape(V):
+    return V.rows, V.cols
+
+
+def _mean(V):
+    """nmf.py:109-112."""
+    n, m = _shape(V)
+    total = float(np.sum(V.values)) if isinstance(V, SparseMatrix) else float(np.sum(V.array))
+    return total / (n * m)
+
+
+def initial_factors(V, cfg):
+    """nmf.py:115-127: seeded U[0,1) factors, G drawn before F."""
+    n, m = _shape(V)
+    rng = np.random.default_rng(cfg.seed)
+    scale = np.sqrt(_mean(V) / cfg.rank)
+    g = np.ascontiguousarray(rng.uniform(size=(n, cfg.rank)) * scale)
+    f = rng.uniform(size=(cfg.rank, m)) * scale
+    ft = np.ascontiguousarray(f.T)
+    return g, ft
+
+
+def build_estep_problem(Q_g, V, col, G, cfg, warm=None):
+    """nmf.py:130-140: H = G^T G + 2 mu2 I, h = -G^T V_col + mu1."""
+    r = Q_g.array.shape[0]
+    H = Q_g.array + (2.0 * cfg.mu2) * np.eye(r)
+    if isinstance(V, SparseMatrix):
+        gtv = sparse_col_times_dense(V, col, G)
+    else:
+        gtv = D.matvec_t_host(G.array, V.array[:, col])
+    h = -gtv + cfg.mu1
+    return NqpProblem(H, h, warm)
+
+
+def build_mstep_problem(H_f, Y, row, cfg, warm=None):
+    """nmf.py:143-149: H = F F^T + 2 beta2 I, h = -Y_row + beta1."""
+    r = H_f.array.shape[0]
+    H = H_f.array + (2.0 * cfg.beta2) * np.eye(r)
+    h = -Y.array[:, row] + cfg.beta1
+    return NqpProblem(H, h, warm)
+
+
+def regularized_objective(V, model, cfg):
+    """nmf.py:152-165, evaluated on the GPU."""
+    g = model.G.array
+    f = model.F.array
+    value = frobenius_objective(V, model.G, model.F)
+    if cfg.mu1 or cfg.beta1 or cfg.mu2 or cfg.beta2:
+        sums = D.abs_sq_sums_host([f, g])
+        if cfg.mu1:
+            value += cfg.mu1 * sums[0][0]
+        if cfg.beta1:
+            value += cfg.beta1 * sums[1][0]
+        if cfg.mu2:
+            value += cfg.mu2 * sums[0][1]
+        if cfg.beta2:
+            value += cfg.beta2 * sums[1][1]
+    return value
+
+
+def _as_matrix(V):
+    if isinstance(V, (DenseMatrix, SparseMatrix)):
+        return V
+    if isinstance(V, torch.Tensor):
+        V = V.detach().cpu().numpy()
+    return DenseMatrix(V)
+
+
+class FitSession:
+    """A prepared fit: data uploaded, factors initialised, loop ready.
+
+    ``run()`` executes the alternation and returns (NmfModel, ConvergenceLog).
+    Splitting preparation from the loop lets callers (bench.py) time the
+    device-resident loop separately from the end-to-end call.
+    """
+
+    def __init__(self, V, cfg, on_iteration=None, init=None, data=None):
+        self.cfg = cfg
+        self.on_iteration = on_iteration
+        if data is None:
+            V = _as_matrix(V)
+            require_nonnegative(V, "data matrix")
+            data = D.DeviceData(V, cfg.precision)
+            n, m = _shape(V)
+            if init is None:
+                init = initial_factors(V, cfg)
+        else:
+            n, m = data.n, data.m
+            if init is None:
+                raise ValueError("init factors required with preloaded device data")
+        self.n, self.m = n, m
+        self.data = data
+        G0, FT0 = init
+        self.state = D.Alternation(data, cfg, G0, FT0, cfg.max_outer, precision=cfg.precision,
+                                   lanes=cfg.lanes)
+
+    def run(self):
+        cfg, st = self.cfg, self.state
+        sync_each = cfg.rel_change_tol > 0.0 or self.on_iteration is not None
+        start = torch.cuda.Event(enable_timing=True)
+        events = []
+        log = ConvergenceLog()
+        start.record()
+        previous = None
+        done = 0
+        xsq = getattr(self.data, "xsq", 0.0)
+        try:
+            for k in range(cfg.max_outer):
+                st.iterate(k)
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                events.append(ev)
+                done = k + 1
+                if sync_each:
+                    ev.synchronize()
+                    stats = st.stats[k].cpu().numpy()
+                    err = st.failure(stats[None], 0)
+                    if err is not None:
+                        raise err
+                    pieces = st.pieces[k].cpu().numpy()
+                    obj = st.assemble(pieces, cfg, self.data.kind, xsq)
+                    log.append(obj, start.elapsed_time(ev) / 1e3, int(stats[:, 0].sum()),
+                               self.m + self.n)
+                    if self.on_iteration is not None:
+                        self.on_iteration(log)
+                    if (cfg.rel_change_tol > 0.0 and previous is not None
+                            and abs(previous - obj)
+                            <= cfg.rel_change_tol * max(abs(previous), 1e-300)):
+                        break
+                    previous = obj
+            if not sync_each:
+                events[-1].synchronize()
+                stats = st.stats[:done].cpu().numpy()
+                pieces = st.pieces[:done].cpu().numpy()
+                for k in range(done):
+                    err = st.failure(stats, k)
+                    if err is not None:
+                        raise err
+                    obj = st.assemble(pieces[k], cfg, self.data.kind, xsq)
+                    log.append(obj, start.elapsed_time(events[k]) / 1e3,
+                               int(stats[k, :, 0].sum()), self.m + self.n)
+        except NumericalFailureError as err:
+            err.log = log
+            raise
+        G, FT = st.factors_host()
+        model = NmfModel(G=DenseMatrix(G), F=DenseMatrix(np.asfortranarray(FT.T)))
+        return model, log
+
+
+def fit(V, cfg, on_iteration=None):
+    """Run the alternation for cfg.max_outer iterations (or until the relative
+    objective change falls below cfg.rel_change_tol) -- nmf.py:168-211.
+
+    Deterministic for a fixed seed.  Raises NumericalFailureError (with the
+    log up to the failure and the failing column/row index) if a subproblem
+    degenerates.
+    """
+    return FitSession(V, cfg, on_iteration=on_iteration).run()

@@ -1,0 +1,229 @@
+"""Nonnegative quadratic programming: minimize 0.5 x'Hx + h'x subject to x >= 0.
+
+Reference API (nqp.py): ``NqpProblem``, ``StopState``, ``rescale``,
+``rescale_arrays``, ``passive_mask``, ``solve``.  The solve itself runs on the
+GPU through libnmfb.so's reference-order kernel (``nmfb_nqp_solve``): the
+anti-lopsided unit-diagonal rescaling (nmfb_rescale, bit-exact against
+nqp.rescale_arrays), then exact line search + greedy coordinate descent with
+the dual stopping rule, recording the per-iteration passive-gradient norm and
+objective histories.  Validation, the two closed-form short-circuits
+(h >= 0, KKT warm start; nqp.py:233-253) and the final unscaled gradient are
+O(r^2) host arithmetic on the single problem.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .exceptions import DegenerateProblemError, NumericalFailureError
+
+DIAG_FREEZE_REL = 1e-12  # nqp.py:33
+DEFAULT_EPSILON = 0.1    # nqp.py:35
+DEFAULT_MAX_INNER = 500  # nqp.py:36
+
+
+@dataclass
+class NqpProblem:
+    """Quadratic form (H, h) with an optional nonnegative warm start (nqp.py:39-69)."""
+
+    H: np.ndarray
+    h: np.ndarray
+    x0: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.H = np.asarray(self.H, dtype=np.float64)
+        self.h = np.asarray(self.h, dtype=np.float64)
+        r = self.h.shape[0]
+        if self.H.shape != (r, r):
+            raise ValueError(f"H must be {r}x{r}, got {self.H.shape}")
+        scale = max(1.0, float(np.max(np.abs(self.H))) if self.H.size else 1.0)
+        if np.max(np.abs(self.H - self.H.T)) > 1e-12 * scale:
+            raise ValueError("H must be symmetric within 1e-12")
+        if np.any(np.diag(self.H) < 0):
+            raise ValueError("diag(H) must be nonnegative")
+        if self.x0 is None:
+            self.x0 = np.zeros(r)
+        else:
+            self.x0 = np.asarray(self.x0, dtype=np.float64)
+            if self.x0.shape != (r,):
+                raise ValueError(f"x0 must have length {r}")
+            if np.any(self.x0 < 0):
+                raise ValueError("x0 must be nonnegative")
+
+    @property
+    def size(self):
+        return self.h.shape[0]
+
+
+@dataclass
+class RescaledProblem:
+    """Unit-diagonal form of an NqpProblem over its active dimensions (nqp.py:72-85)."""
+
+    Q: np.ndarray
+    q: np.ndarray
+    scale: np.ndarray
+    active_dims: np.ndarray
+
+
+@dataclass
+class NqpSolution:
+    x: np.ndarray
+    grad: np.ndarray
+    inner_iterations: int
+    initial_passive_grad_norm_sq: float
+    final_passive_grad_norm_sq: float
+    passive_grad_norm_history: np.ndarray
+    objective_history: np.ndarray
+
+
+@dataclass
+class StopState:
+    """Per-worker stopping state (nqp.py:98-113)."""
+
+    epsilon: float = DEFAULT_EPSILON
+    max_stop: float = 0.0
+
+    def __post_init__(self):
+        if not 0.0 <= self.epsilon <= 1.0:
+            raise ValueError("epsilon must lie in [0, 1]")
+        if self.max_stop < 0.0:
+            raise ValueError("max_stop must be >= 0")
+
+    def update(self, final_norm_sq):
+        self.max_stop = max(self.max_stop, float(final_norm_sq))
+
+
+def _device_rescale(H, diag_add=0.0):
+    """nmfb_rescale on the GPU -> (scale, active, Qa compact, device buffers)."""
+    import torch
+
+    from . import _lib as L
+    from . import device as D
+
+    dev = D.require_cuda()
+    r = H.shape[0]
+    Hd = torch.from_numpy(np.ascontiguousarray(H, dtype=np.float64)).to(dev)
+    bufs = dict(Qa=torch.zeros((max(r * r, 1),), dtype=torch.float64, device=dev),
+                sa=torch.zeros((r,), dtype=torch.float64, device=dev),
+                act=torch.zeros((r,), dtype=torch.int32, device=dev),
+                active=torch.zeros((r,), dtype=torch.uint8, device=dev),
+                ra=torch.zeros((1,), dtype=torch.int32, device=dev),
+                scale=torch.zeros((r,), dtype=torch.float64, device=dev))
+    L.call("nmfb_rescale", L.F64, D.vp(Hd), r, float(diag_add), D.vp(bufs["Qa"]),
+           D.vp(bufs["sa"]), D.vp(bufs["act"]), D.vp(bufs["active"]), D.vp(bufs["ra"]),
+           D.vp(bufs["scale"]), D.stream_handle())
+    ra = int(bufs["ra"].item())
+    active = bufs["active"].cpu().numpy().astype(bool)
+    Qa = bufs["Qa"][: ra * ra].cpu().numpy().reshape(ra, ra)
+    return bufs["scale"].cpu().numpy(), active, Qa, bufs
+
+
+def rescale_arrays(H):
+    """(scale, active mask, unit-diagonal Q) for a raw H (nqp.py:116-131).
+    Computed by the GPU rescale kernel (bit-exact with the reference)."""
+    H = np.asarray(H, dtype=np.float64)
+    r = H.shape[0]
+    if r == 0:
+        return np.zeros(0), np.zeros(0, dtype=bool), np.zeros((0, 0))
+    scale, active, Qa, _ = _device_rescale(H)
+    Q = np.zeros((r, r))
+    idx = np.flatnonzero(active)
+    Q[np.ix_(idx, idx)] = Qa
+    return scale, active, Q
+
+
+def rescale(p: NqpProblem) -> RescaledProblem:
+    """nqp.py:134-143; raises DegenerateProblemError if every dim is frozen."""
+    scale, active, Q = rescale_arrays(p.H)
+    if not active.any():
+        raise DegenerateProblemError(
+            "all diagonal entries are numerically zero; objective is linear in every variable")
+    q = np.where(active, p.h / np.where(active, scale, 1.0), 0.0)
+    return RescaledProblem(Q=Q, q=q, scale=scale, active_dims=active)
+
+
+def passive_mask(x, grad):
+    """Coordinates free to move: positive value or negative gradient (nqp.py:146-148)."""
+    return (x > 0) | (grad < 0)
+
+
+def _passive_norm_sq(x, grad):
+    d = np.where(passive_mask(x, grad), grad, 0.0)
+    return float(d @ d)
+
+
+def solve(p: NqpProblem, stop: StopState | None = None, max_inner: int = DEFAULT_MAX_INNER,
+          check_gradients: bool = False) -> NqpSolution:
+    """Solve an NQP problem to the accuracy governed by ``stop`` (nqp.py:217-320).
+
+    The iterative solve runs on the GPU (reference-order fp64 kernel).
+    ``check_gradients`` verifies the final incremental gradient against a
+    fresh Q y + q (the reference checks every iteration).
+    """
+    import torch
+
+    from . import _lib as L
+    from . import device as D
+
+    if stop is None:
+        stop = StopState()
+    if max_inner < 1:
+        raise ValueError("max_inner must be >= 1")
+    r = p.size
+    if np.all(p.h >= 0.0):
+        stop.update(0.0)
+        return NqpSolution(x=np.zeros(r), grad=p.h.copy(), inner_iterations=0,
+                           initial_passive_grad_norm_sq=0.0, final_passive_grad_norm_sq=0.0,
+                           passive_grad_norm_history=np.zeros(1), objective_history=np.zeros(1))
+    grad0 = p.H @ p.x0 + p.h
+    if _passive_norm_sq(p.x0, grad0) == 0.0:
+        stop.update(0.0)
+        f0 = float(0.5 * p.x0 @ grad0 + 0.5 * p.h @ p.x0)
+        return NqpSolution(x=p.x0.copy(), grad=grad0, inner_iterations=0,
+                           initial_passive_grad_norm_sq=0.0, final_passive_grad_norm_sq=0.0,
+                           passive_grad_norm_history=np.zeros(1),
+                           objective_history=np.asarray([f0]))
+    scale, active, Qa, bufs = _device_rescale(p.H)
+    if not active.any():
+        raise DegenerateProblemError(
+            "all diagonal entries are numerically zero; objective is linear in every variable")
+    if np.any(p.h[~active] < 0.0):
+        frozen = int(np.flatnonzero(~active & (p.h < 0.0))[0])
+        raise NumericalFailureError(
+            f"objective is unbounded along degenerate dimension {frozen} "
+            f"(zero curvature, negative slope)", last_x=p.x0.copy())
+    dev = bufs["Qa"].device
+    h = torch.from_numpy(p.h.copy()).to(dev)
+    x = torch.from_numpy(p.x0.copy()).to(dev)
+    iters = torch.zeros((1,), dtype=torch.int32, device=dev)
+    final = torch.zeros((1,), dtype=torch.float64, device=dev)
+    hist = torch.zeros((max_inner + 1, 2), dtype=torch.float64, device=dev)
+    stats = torch.tensor([0, -1], dtype=torch.int64, device=dev)
+    L.call("nmfb_nqp_solve", D.vp(bufs["Qa"]), D.vp(bufs["sa"]), D.vp(bufs["act"]),
+           D.vp(bufs["active"]), r, D.vp(bufs["ra"]), D.vp(h), D.vp(x), 1,
+           float(stop.epsilon), int(max_inner), float(stop.max_stop), D.vp(iters), D.vp(final),
+           D.vp(hist), max_inner + 1, D.vp(stats), D.stream_handle())
+    it = int(iters.item())
+    if it < 0:
+        raise NumericalFailureError(f"NaN/Inf after inner iterations (max {max_inner})",
+                                    last_x=p.x0.copy())
+    xs = x.cpu().numpy()
+    hh = hist.cpu().numpy()[: it + 1]
+    norm0 = float(hh[0, 0])
+    norm_k = float(final.item())
+    if check_gradients:
+        idx = np.flatnonzero(active)
+        y = xs[idx] * scale[idx]
+        qa = p.h[idx] / scale[idx]
+        fresh = Qa @ y + qa
+        gy = (p.H @ xs + p.h)[idx] / scale[idx]
+        ref = max(1.0, float(np.max(np.abs(fresh))))
+        if np.max(np.abs(gy - fresh)) > 1e-9 * ref:
+            raise AssertionError("incremental gradient drifted from Qx + q")
+    stop.update(norm_k)
+    return NqpSolution(x=xs, grad=p.H @ xs + p.h, inner_iterations=it,
+                       initial_passive_grad_norm_sq=norm0, final_passive_grad_norm_sq=norm_k,
+                       passive_grad_norm_history=hh[:, 0].copy(),
+                       objective_history=hh[:, 1].copy())

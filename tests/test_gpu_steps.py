@@ -1,0 +1,108 @@
+"""GPU parity of the coefficient / component steps and of the drop-in shard
+kernels, against the reference's own outputs (tests/golden/steps.npz) and the
+oracle.  fp64 check mode: bit-exact, including the per-worker reduce order."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import nmf_oracle as orc
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+STEPS = np.load(os.path.join(GOLD, "steps.npz"))
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {
+    "plain_w1": dict(workers=1),
+    "plain_w3": dict(workers=3),
+    "reg_w1": dict(workers=1, mu1=0.05, mu2=0.02, beta1=0.03, beta2=0.01),
+    "reg_w3": dict(workers=3, mu1=0.05, mu2=0.02, beta1=0.03, beta2=0.01),
+}
+
+
+def _data(kind):
+    from paper_1506_08938_b200 import SparseMatrix
+
+    arr = STEPS["data/arr"]
+    return arr, (SparseMatrix.from_dense(arr) if kind == "sparse" else np.ascontiguousarray(arr.T))
+
+
+@pytest.mark.parametrize("kind", ["dense", "sparse"])
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_run_estep_mstep_fp64_bit_exact(kind, variant):
+    from paper_1506_08938_b200 import NmfConfig
+    from paper_1506_08938_b200.parallel import run_estep, run_mstep
+
+    arr, V = _data(kind)
+    g0, ft0 = STEPS["data/g"], STEPS["data/ft"]
+    cfg = NmfConfig(rank=g0.shape[1], seed=0, precision="fp64", **VARIANTS[variant])
+    p = f"{kind}/{variant}"
+    G, FT = g0.copy(), ft0.copy()
+    Y, H_f, e = run_estep(V, G, STEPS[p + "/Q_g"], cfg, FT)
+    assert np.array_equal(FT, STEPS[p + "/FT"])
+    assert np.array_equal(np.ascontiguousarray(Y.array), STEPS[p + "/Y"])
+    assert np.array_equal(np.ascontiguousarray(H_f.array), STEPS[p + "/H_f"])
+    assert e.inner_iterations == int(STEPS[p + "/e_inner"])
+    m = run_mstep(Y, H_f, cfg, G)
+    assert np.array_equal(G, STEPS[p + "/G"])
+    assert m.inner_iterations == int(STEPS[p + "/m_inner"])
+
+
+@pytest.mark.parametrize("kind", ["dense", "sparse"])
+def test_run_estep_fp32_close(kind):
+    from gpu_util import floored_rel
+
+    from paper_1506_08938_b200 import NmfConfig
+    from paper_1506_08938_b200.parallel import run_estep, run_mstep
+
+    arr, V = _data(kind)
+    g0, ft0 = STEPS["data/g"], STEPS["data/ft"]
+    cfg = NmfConfig(rank=g0.shape[1], seed=0, precision="fp32")
+    p = f"{kind}/plain_w1"
+    G, FT = g0.copy(), ft0.copy()
+    Y, H_f, e = run_estep(V, G, STEPS[p + "/Q_g"], cfg, FT)
+    assert floored_rel(FT, STEPS[p + "/FT"]) < 1e-2
+    np.testing.assert_allclose(np.ascontiguousarray(Y.array), STEPS[p + "/Y"], rtol=1e-3,
+                               atol=1e-4 * np.abs(STEPS[p + "/Y"]).max())
+    m = run_mstep(Y, H_f, cfg, G)
+    assert floored_rel(G, STEPS[p + "/G"]) < 1e-2
+
+
+@pytest.mark.parametrize("kind", ["dense", "sparse"])
+@pytest.mark.parametrize("lo,hi", [(0, 150), (32, 96), (7, 130)])
+def test_dropin_shard_kernels_fp64_bit_exact(kind, lo, hi):
+    """paper_1506_08938_b200.kernels.* == oracle (== reference) shard calls."""
+    from paper_1506_08938_b200 import kernels
+
+    arr = STEPS["data/arr"]
+    g0, ft0 = STEPS["data/g"], STEPS["data/ft"]
+    n, m = arr.shape
+    r = g0.shape[1]
+    Q_g = orc.gram(g0)
+    sa, act, idx, Qa = orc.rescale_for_step(Q_g + 0.04 * np.eye(r))
+    args = (Qa, sa, idx, act, 0.05, 0.1, 500, 0.5)
+    FT1, YT1, HP1 = ft0.copy(), np.zeros((n, r)), np.zeros((r, r))
+    FT2, YT2, HP2 = ft0.copy(), np.zeros((n, r)), np.zeros((r, r))
+    if kind == "dense":
+        VT = np.ascontiguousarray(arr.T)
+        want = orc.estep_dense(VT, lo, hi, g0, *args, FT1, YT1, HP1)
+        got = kernels.estep_dense(VT, lo, hi, g0, *args, FT2, YT2, HP2)
+    else:
+        V = orc.Csc.from_dense(arr)
+        want = orc.estep_sparse(V.indptr, V.indices, V.values, lo, hi, g0, *args, FT1, YT1, HP1)
+        got = kernels.estep_sparse(V.indptr, V.indices, V.values, lo, hi, g0, *args, FT2, YT2,
+                                   HP2)
+    assert got == want
+    assert np.array_equal(FT2, FT1)
+    assert np.array_equal(YT2, YT1)
+    assert np.array_equal(HP2, HP1)
+    # component step on the accumulated Y^T
+    G1, G2 = g0.copy(), g0.copy()
+    sa2, act2, idx2, Qa2 = orc.rescale_for_step(orc.gram(FT1) + 0.02 * np.eye(r))
+    margs = (Qa2, sa2, idx2, act2, 0.01, 0.1, 500, 0.0)
+    want = orc.mstep_rows(YT1, 3, n, *margs, G1)
+    got = kernels.mstep_rows(YT1, 3, n, *margs, G2)
+    assert got == want
+    assert np.array_equal(G2, G1)
