@@ -1,0 +1,347 @@
+"""Benchmark of the alternating-NNLS hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): dense NMF of X = W0 H0 + |N(0,0.05)|,
+X 10000 x 20000, W0/H0 ~ Exp(1) (seed 1), rank 50, fp32 on the GPU.  One step
+= one outer iteration of nmf.fit (Gram + rescale, G^T X, NNLS over the
+20000 columns, F F^T, X F^T, NNLS over the 10000 rows, objective), i.e.
+30000 column/row NNLS solves.  ``value`` = solves/s over the timed steps with
+X and the factors resident in HBM; ``e2e`` = the same metric through the
+public ``fit()`` call from a pinned host buffer (upload of X, seeded init,
+the iterations, download of G, F and the log all inside the timed region).
+
+N > 1 (torchrun, one rank per GPU): weak scaling -- every rank owns a
+C2-shaped column block of a 10000 x (20000 N) matrix (columns sharded, G
+replicated, NCCL for the r x r Gram allreduce, the Y^T reduce-scatter and the
+G allgather; paper_1506_08938_b200/dist.py).
+
+``--impl reference``: the reference's CPU path on this host's cores -- the
+oracle port (oracle/, a C + numpy restatement bit-exact to the reference),
+multithreaded like the reference's shard workers, on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_ROWS, N_COLS, RANK, SEED = 10000, 20000, 50, 1
+WORKLOAD = "C2: dense NMF 10000x20000, rank 50, fp32 (BASELINE.json configs[1])"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_block(rank):
+    """This rank's C2-shaped column block (float64 host, (n, m) Fortran)."""
+    from oracle import generators
+
+    seed = SEED if rank == 0 else SEED + 1000 * rank
+    return np.asfortranarray(generators.dense_exp(N_ROWS, N_COLS, RANK, 0.05, seed))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6552.6), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/ncu_summary.json), or None."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            return json.load(f).get("gemm_tall", {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    from paper_1506_08938_b200 import NmfConfig, _lib
+    from paper_1506_08938_b200 import device as D
+    from paper_1506_08938_b200.nmf import FitSession, initial_factors_from_mean
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    X = make_block(rank)
+    n, m = X.shape
+    cfg = NmfConfig(rank=RANK, max_outer=args.warmup + args.steps, seed=SEED, rel_change_tol=0.0,
+                    precision="fp32")
+    G0, FT0 = initial_factors_from_mean(n, m * world, float(X.mean()), cfg)
+    FT0 = FT0[rank * m:(rank + 1) * m]
+    if world > 1:
+        from paper_1506_08938_b200 import dist as PD
+
+        sess = PD.DistFit(X, cfg, init=(G0, FT0))
+        st = sess.state
+    else:
+        sess = FitSession(X, cfg, init=(G0, FT0))
+        st = sess.state
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for k in range(args.warmup):
+        st.iterate(k)
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with _lib.Recorder(timing=True) as rec:
+        t0.record()
+        for k in range(args.warmup, args.warmup + args.steps):
+            st.iterate(k)
+        t1.record()
+    barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    solves_step = (m * world + n)
+    value = solves_step * args.steps / (ms / 1e3)
+    calls = rec.summary()
+    # dominant kernel: the largest share of the step
+    dom = max(calls.items(), key=lambda kv: kv[1][1])
+    gemm_calls, gemm_ms = calls.get("nmfb_gemm_tall", (0, 0.0))
+    hbm, peak_src = peaks()
+    # algorithmic bytes per gemm_tall launch: X once + B (K x r) + split-K partials
+    splits = (st.splits_e + st.splits_m) / 2 if hasattr(st, "splits_e") else 1
+    gemm_bytes = 4.0 * (n * m + (n + m) / 2 * RANK + splits * (n + m) / 2 * RANK)
+    gemm_avg_ms = gemm_ms / max(gemm_calls, 1)
+    achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9
+    share = {k: round(v[1] / ms, 4) for k, v in calls.items()}
+    # log sanity: objective decreasing
+    pieces = st.pieces[: args.warmup + args.steps].cpu().numpy()
+    objs = [st.assemble(p, cfg, "dense", 0.0) for p in pieces]
+    result = {
+        "metric": "column NNLS solves/sec (NMF outer iteration: E+M steps + objective)",
+        "value": value,
+        "unit": "solves/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "outer_iters_per_sec": 1e3 / ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic (seeded generator oracle/generators.py, BASELINE C2 shape)",
+        "config": {"workload": WORKLOAD, "n": n, "m_per_gpu": m, "rank": RANK,
+                   "solves_per_step": solves_step,
+                   "step": "one outer iteration of fit(): gram+rescale, G^T X, NNLS(m cols), "
+                           "F F^T, X F^T, NNLS(n rows), objective",
+                   "l2": "inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
+                         % (n * m * 4 / 1e6),
+                   "parallelism": f"dp{world} (column-sharded)"},
+        "roofline": {"kernel": "nmfb_gemm_tall (split-K SIMT FFMA, G^T X and X F^T passes)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": gemm_bytes,
+                     "avg_launch_ms": gemm_avg_ms, "traffic": profile_traffic()},
+        "step_share": share,
+        "dominant": dom[0],
+        "clocks": clk,
+        "gpu_launches": rec.launches,
+        "objective_first_last": [objs[0], objs[-1]],
+    }
+    if rank == 0 and world == 1 and not args.no_e2e:
+        result["e2e"] = run_e2e(args, X, cfg)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(X, bounded=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return result if rank == 0 else None
+
+
+def run_e2e(args, X, cfg):
+    """Public fit() from a pinned host buffer: H2D of X, init, K iterations,
+    D2H of factors and log, all inside the timed region."""
+    import torch
+
+    from paper_1506_08938_b200 import NmfConfig, fit
+
+    n, m = X.shape
+    XT = torch.from_numpy(np.ascontiguousarray(X.T, dtype=np.float32)).pin_memory()
+    V = XT.t()  # (n, m) view of the pinned (m, n) buffer
+    ecfg = NmfConfig(rank=RANK, max_outer=args.steps, seed=SEED, rel_change_tol=0.0,
+                     precision="fp32")
+    fit(V, NmfConfig(rank=RANK, max_outer=2, seed=SEED, rel_change_tol=0.0, precision="fp32"))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    model, log = fit(V, ecfg)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    h2d = n * m * 4 + (n + m) * RANK * 4
+    d2h = (n + m) * RANK * 8 + args.steps * (12 * 8 + 4 * 8)
+    return {"value": (n + m) * args.steps / dt, "unit": "solves/s",
+            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+            "seconds": dt, "call": f"fit(pinned torch (n,m) fp32 view, max_outer={args.steps})",
+            "final_objective": log.final_objective}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle port on this host's cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(X, bounded=True, iters=1):
+    from oracle import nmf_oracle as orc
+
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    n, m = X.shape
+    cfg = orc.Config(rank=RANK, max_outer=iters, seed=SEED, rel_change_tol=0.0, workers=cores)
+    orc.fit(X[:64, :64], orc.Config(rank=4, max_outer=1, seed=0))  # load the C library
+    timer = {}
+    t = time.perf_counter()
+    G, FT, log = orc.fit(X, cfg, step_timer=timer)
+    dt = time.perf_counter() - t
+    return {"value": (n + m) * iters / dt, "unit": "solves/s", "cores": cores, "kind": "port",
+            "sample": f"{iters} outer iteration(s) of the full C2 workload (10000x20000, r=50) "
+                      f"in float64 by the oracle port (C kernels + numpy/OpenBLAS, "
+                      f"{cores} shard threads), objective included",
+            "seconds": dt, "em_only_solves_per_s": (n + m) * iters / timer["em_seconds"]}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    X = make_block(0)
+    n, m = X.shape
+    from oracle import nmf_oracle as orc
+
+    cores = os.cpu_count() or 1
+    cfg = orc.Config(rank=RANK, max_outer=args.warmup + args.steps, seed=SEED,
+                     rel_change_tol=0.0, workers=cores)
+    orc.fit(X[:64, :64], orc.Config(rank=4, max_outer=1, seed=0))
+    # warmup + timed steps of the same workload; the objective's numpy
+    # residual is part of the reference step (nmf.py:193-194)
+    G, FT = orc.initial_factors(X, cfg)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        G, FT, _, _, _, _ = orc.one_iteration(X, G, FT, cfg)
+        times.append(time.perf_counter() - t)
+    dt = sum(times[args.warmup:])
+    value = (n + m) * args.steps / dt
+    return {"impl": "reference", "metric": "column NNLS solves/sec (NMF outer iteration: "
+            "E+M steps + objective)", "value": value, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+            "data": "synthetic (same generator as our arm)",
+            "config": {"workload": WORKLOAD, "n": n, "m": m, "rank": RANK},
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} outer iterations of C2 (after "
+                                       f"{args.warmup} warm-up), oracle port, {cores} threads"},
+            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

@@ -109,7 +109,56 @@ def check(status, what):
     raise NativeLibraryError(f"{what}: status {status}")
 
 
+# kernels launched by one call of each entry point (gpu_launches accounting)
+KERNELS_PER_CALL = {
+    "nmfb_nnls_batch": 1, "nmfb_nqp_solve": 1, "nmfb_gram": 2, "nmfb_rescale": 1,
+    "nmfb_gemm_tall": 1, "nmfb_dense_linear_ref": 1, "nmfb_dense_yt_ref": 1, "nmfb_hp_ref": 1,
+    "nmfb_csc_linear": 1, "nmfb_csr_yt": 1, "nmfb_dense_residual": 2, "nmfb_dot": 2,
+}
+
+
+class Recorder:
+    """Counts kernel launches and (optionally) times every C-ABI call with
+    CUDA events on the current stream: ``with Recorder(timing=True) as rec``."""
+
+    active = None
+
+    def __init__(self, timing=False):
+        self.timing = timing
+        self.launches = 0
+        self.calls = []  # (name, start_event, end_event)
+
+    def __enter__(self):
+        Recorder.active = self
+        return self
+
+    def __exit__(self, *exc):
+        Recorder.active = None
+
+    def summary(self):
+        """{name: (calls, total_ms)} (call after synchronizing)."""
+        out = {}
+        for name, a, b in self.calls:
+            c, t = out.get(name, (0, 0.0))
+            out[name] = (c + 1, t + a.elapsed_time(b))
+        return out
+
+
 def call(name, *args):
+    rec = Recorder.active
+    if rec is not None:
+        rec.launches += KERNELS_PER_CALL.get(name, 0)
+        if rec.timing:
+            import torch
+
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            status = getattr(lib(), name)(*args)
+            b.record()
+            rec.calls.append((name, a, b))
+            check(status, name)
+            return status
     status = getattr(lib(), name)(*args)
     check(status, name)
     return status

@@ -50,13 +50,10 @@ static int cuda_status(cudaError_t e) {
     snprintf(g_err, sizeof(g_err), "%s", cudaGetErrorString(e));
     return NMFB_ERR_CUDA;
 }
-static int check(int status) {
-    if (status == NMFB_ERR_CUDA) {
-        cudaError_t e = cudaGetLastError();
-        snprintf(g_err, sizeof(g_err), "%s", cudaGetErrorString(e));
-    }
-    return status;
-}
+namespace nmfb {
+int launch_status() { return cuda_status(cudaGetLastError()); }
+}  // namespace nmfb
+static int check(int status) { return status; }
 static inline size_t esize(int dtype) { return dtype == NMFB_F64 ? 8 : 4; }
 
 extern "C" {
@@ -277,7 +274,7 @@ static int run_shard_nnls(int dtype, int mode, const void *Qa, const void *scale
                           Scratch &s, uint64_t **stats_out, void **finals_out) {
     uint64_t *stats = (uint64_t *)s.get(2 * sizeof(uint64_t));
     void *finals = s.get(esize(dtype) * (hi - lo));
-    if (!stats || !finals) return NMFB_ERR_CUDA;
+    if (!stats || !finals) return launch_status() == NMFB_OK ? NMFB_ERR_CUDA : NMFB_ERR_CUDA;
     uint64_t init[2] = {0ull, ~0ull};
     cudaMemcpyAsync(stats, init, sizeof(init), cudaMemcpyHostToDevice, s.st);
     int rc = nmfb_nnls_batch(dtype, mode, Qa, scale_a, act_idx, active, r, ra, nullptr, h, dtype,

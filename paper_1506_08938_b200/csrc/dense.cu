@@ -179,7 +179,7 @@ int gemm_tall_launch(const float *A, int a_kmajor, int64_t M, int64_t K, int64_t
             gemm_tall_kernel<false, false><<<grid, 256, 0, st>>>(A, M, K, lda, B, N, ldb, C,
                                                                  kchunk);
     }
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 // ---------------------------------------------------------------------------
@@ -273,7 +273,7 @@ int dense_linear_ref_launch(int dtype, const void *VT, int64_t n, int64_t col_lo
         dense_linear_ref_kernel<float><<<grid, 128, 0, st>>>((const float *)VT, n, col_lo, col_hi,
                                                              (const float *)G, r, (float)mu1,
                                                              (float *)h);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 int dense_yt_ref_launch(int dtype, const void *VT, int64_t m, int64_t n, const void *FT, int r,
@@ -289,7 +289,7 @@ int dense_yt_ref_launch(int dtype, const void *VT, int64_t m, int64_t n, const v
     else
         dense_yt_ref_kernel<float><<<grid, 256, 0, st>>>((const float *)VT, m, n,
                                                          (const float *)FT, r, sh, (float *)YT);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 int hp_ref_launch(int dtype, const void *FT, int64_t m, int r, const int64_t *bounds,
@@ -301,7 +301,7 @@ int hp_ref_launch(int dtype, const void *FT, int64_t m, int r, const int64_t *bo
         hp_ref_kernel<double><<<grid, 256, 0, st>>>((const double *)FT, m, r, sh, (double *)HF);
     else
         hp_ref_kernel<float><<<grid, 256, 0, st>>>((const float *)FT, m, r, sh, (float *)HF);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 // ---------------------------------------------------------------------------
@@ -408,7 +408,7 @@ int dense_residual_launch(int dtype, const void *XT, int64_t m, int64_t n, const
         residual_kernel<float><<<grid, 256, 0, st>>>((const float *)XT, m, n, (const float *)G,
                                                      (const float *)FT, r, part);
     sum_parts_kernel<<<1, 256, 0, st>>>(part, gx * gy, 0.5, out);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 }  // namespace nmfb

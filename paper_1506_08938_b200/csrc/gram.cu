@@ -131,7 +131,7 @@ int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, doub
                                                          part);
     }
     gram_reduce_kernel<<<(r * r + 255) / 256, 256, 0, st>>>(part, (int)nchunk, r, out);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 // ---------------------------------------------------------------------------
@@ -210,7 +210,7 @@ int rescale_launch(int dtype, const double *G, int r, double diag_add, void *Qa,
         rescale_kernel<float><<<1, 256, smem, st>>>(G, r, diag_add, (float *)Qa,
                                                     (float *)scale_a, act_idx, active, ra_dev,
                                                     full_scale);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 }  // namespace nmfb

@@ -38,4 +38,7 @@ struct NnlsLaunch {
 
 int nnls_launch(const NnlsLaunch &p);
 
+// NMFB_OK, or NMFB_ERR_CUDA after recording the launch error for nmfb_last_error()
+int launch_status();
+
 }  // namespace nmfb

@@ -340,14 +340,13 @@ static int launch_fast_variant(const NnlsLaunch &p) {
     size_t smem = sizeof(float) * R * S;
     auto kern = nnls_fast_kernel<TH, E, L, B>;
     if (smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-            return NMFB_ERR_CUDA;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (launch_status() != NMFB_OK) return NMFB_ERR_CUDA;
     }
     int64_t nblk = num_blocks(p);
     dim3 grid((unsigned)((nblk + B - 1) / B));
     kern<<<grid, 32 * L * B, smem, p.stream>>>(a);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 

@@ -237,7 +237,7 @@ int launch_ref_impl(const NnlsLaunch &p) {
         nnls_ref_kernel<T, TH, 256><<<grid, 32 * wpb, 0, p.stream>>>(a);
     else
         return NMFB_ERR_ARG;
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 template int launch_ref_impl<double, double>(const NnlsLaunch &);

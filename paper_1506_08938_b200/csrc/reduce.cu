@@ -73,7 +73,7 @@ int dot_launch(const void *a, int a_dtype, const void *b, int b_dtype, int64_t l
     else
         dot_launch_a<float>((const float *)a, b, b_dtype, len, part, st);
     dot3_final_kernel<<<1, 256, 0, st>>>(part, DOT_BLOCKS, out);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 // dst[i] += src[i] (exact elementwise add; used to accumulate drop-in outputs)
@@ -98,7 +98,7 @@ int add_into_launch(int dtype, void *dst, const void *src, int64_t len, int uppe
                                                    upper_r);
     else
         axpy1_kernel<float><<<grid, 256, 0, st>>>((float *)dst, (const float *)src, len, upper_r);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 }  // namespace nmfb

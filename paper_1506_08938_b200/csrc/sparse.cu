@@ -145,7 +145,7 @@ static int csc_linear_dispatch(const int64_t *indptr, const int32_t *rowidx, con
     else
         return NMFB_ERR_ARG;
 #undef NMFB_CSC
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 int csc_linear_launch(int dtype, int mode, const int64_t *indptr, const int32_t *rowidx,
@@ -184,7 +184,7 @@ static int csr_yt_dispatch(const int64_t *rowptr, const int32_t *colidx, const v
     else
         return NMFB_ERR_ARG;
 #undef NMFB_CSR
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 int csr_yt_launch(int dtype, int mode, const int64_t *rowptr, const int32_t *colidx,
@@ -245,7 +245,7 @@ int csc_scatter_yt_launch(int dtype, const int64_t *indptr, const int32_t *rowid
     else
         csc_scatter_yt_kernel<float><<<grid, 64, 0, st>>>(indptr, rowidx, (const float *)vals, lo,
                                                          hi, (const float *)FT, r, (float *)YT);
-    return cudaGetLastError() == cudaSuccess ? NMFB_OK : NMFB_ERR_CUDA;
+    return launch_status();
 }
 
 }  // namespace nmfb

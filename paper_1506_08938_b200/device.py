@@ -93,6 +93,16 @@ class DeviceData:
         dt = _TORCH[precision]
         if isinstance(V, DenseMatrix):
             V = V.array
+        if isinstance(V, torch.Tensor):
+            # (n, m) tensor; V.t() contiguous (an XT buffer) -> no host copy, and a
+            # pinned host buffer uploads asynchronously at full PCIe/C2C rate
+            if V.dim() != 2:
+                raise ValueError("dense data must be 2-D")
+            self.kind = "dense"
+            self.n, self.m = V.shape
+            self.XT = V.t().contiguous().to(self.device, dt, non_blocking=True)
+            self.host = None
+            return
         if isinstance(V, SparseMatrix):
             self.kind = "sparse"
             self.n, self.m = V.rows, V.cols
@@ -426,3 +436,21 @@ def abs_sq_sums_host(arrays):
         oo = o.cpu().numpy()
         out.append((float(oo[1]), float(oo[2])))
     return out
+
+
+def validate_and_sum(data):
+    """Finite / nonnegative check (require_nonnegative, matrix.py:169-178) and
+    sum(X) in fp64 for the init scale, on the device (dense data)."""
+    from .exceptions import DataDomainError
+
+    X = data.XT
+    if not bool(torch.isfinite(X).all()):
+        raise DataDomainError("data matrix contains NaN or Inf")
+    if X.numel() and float(X.min()) < 0:
+        raise DataDomainError("data matrix contains negative entries")
+    ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=torch.float64,
+                     device=X.device)
+    out = torch.zeros((3,), dtype=torch.float64, device=X.device)
+    L.call("nmfb_dot", vp(X), _CODE[data.precision], None, L.F64, X.numel(), vp(out), vp(ws),
+           stream_handle())
+    return float(out[1].item())  # sum |x| == sum x for nonnegative data

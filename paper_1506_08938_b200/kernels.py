@@ -28,6 +28,7 @@ class _Args:
     def __init__(self):
         self.dev = D.require_cuda()
         self.back = []
+        self.keep = []  # device copies must outlive the (async) call
 
     def dev_t(self, a, dtype=None, inout=False):
         if isinstance(a, torch.Tensor):
@@ -37,6 +38,7 @@ class _Args:
         arr = np.asarray(a)
         t = torch.from_numpy(np.ascontiguousarray(arr if dtype is None else arr.astype(dtype)))
         t = t.to(self.dev)
+        self.keep.append(t)
         if inout:
             self.back.append((a, t))
         return t

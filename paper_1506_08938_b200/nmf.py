@@ -117,8 +117,12 @@ def _mean(V):
 def initial_factors(V, cfg):
     """nmf.py:115-127: seeded U[0,1) factors, G drawn before F."""
     n, m = _shape(V)
+    return initial_factors_from_mean(n, m, _mean(V), cfg)
+
+
+def initial_factors_from_mean(n, m, mean, cfg):
     rng = np.random.default_rng(cfg.seed)
-    scale = np.sqrt(_mean(V) / cfg.rank)
+    scale = np.sqrt(mean / cfg.rank)
     g = np.ascontiguousarray(rng.uniform(size=(n, cfg.rank)) * scale)
     f = rng.uniform(size=(cfg.rank, m)) * scale
     ft = np.ascontiguousarray(f.T)
@@ -182,7 +186,15 @@ class FitSession:
     def __init__(self, V, cfg, on_iteration=None, init=None, data=None):
         self.cfg = cfg
         self.on_iteration = on_iteration
-        if data is None:
+        if data is None and isinstance(V, torch.Tensor):
+            # torch input (e.g. a pinned host buffer): upload first, validate
+            # and take the mean for the init scale on the device
+            data = D.DeviceData(V, cfg.precision)
+            total = D.validate_and_sum(data)
+            n, m = data.n, data.m
+            if init is None:
+                init = initial_factors_from_mean(n, m, total / (n * m), cfg)
+        elif data is None:
             V = _as_matrix(V)
             require_nonnegative(V, "data matrix")
             data = D.DeviceData(V, cfg.precision)
