@@ -151,7 +151,8 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = "WORLD_SIZE" in os.environ  # torchrun: NCCL path even at 1 rank
+    if use_dist:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -161,7 +162,7 @@ def run_ours(args):
                     precision="fp32")
     G0, FT0 = initial_factors_from_mean(n, m * world, float(X.mean()), cfg)
     FT0 = FT0[rank * m:(rank + 1) * m]
-    if world > 1:
+    if use_dist:
         from paper_1506_08938_b200 import dist as PD
 
         sess = PD.DistFit(X, cfg, init=(G0, FT0))
@@ -172,7 +173,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     def barrier():
-        if world > 1:
+        if use_dist:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -191,7 +192,7 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
@@ -248,7 +249,7 @@ def run_ours(args):
         result["e2e"] = run_e2e(args, X, cfg)
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(X, bounded=True)
-    if world > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
     return result if rank == 0 else None
 

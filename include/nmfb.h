@@ -192,6 +192,10 @@ size_t nmfb_residual_workspace_bytes(int64_t m, int64_t n);
 int nmfb_dense_residual(int dtype, const void *XT, int64_t m, int64_t n, const void *G,
                         const void *FT, int32_t r, double *out, void *workspace, void *stream);
 
+/* out[i] = sum_{s < S} parts[s * len + i], fixed order (split-K partials of
+ * X F^T summed before the multi-GPU reduce-scatter).  float32. */
+int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void *stream);
+
 /* out[0] = sum a_i * b_i, out[1] = sum |a_i|, out[2] = sum a_i^2 (fp64,
  * deterministic).  b may be NULL (then out[0] = 0).  a_dtype / b_dtype. */
 size_t nmfb_dot_workspace_bytes(int64_t len);

@@ -36,6 +36,7 @@ int dot_launch(const void *a, int a_dtype, const void *b, int b_dtype, int64_t l
                void *ws, cudaStream_t st);
 int add_into_launch(int dtype, void *dst, const void *src, int64_t len, int upper_r,
                     cudaStream_t st);
+int sum_parts_launch(const float *parts, int S, int64_t len, float *out, cudaStream_t st);
 int csc_scatter_yt_launch(int dtype, const int64_t *indptr, const int32_t *rowidx,
                           const void *vals, int64_t lo, int64_t hi, const void *FT, int r,
                           void *YT, cudaStream_t st);
@@ -208,6 +209,10 @@ int nmfb_dense_residual(int dtype, const void *XT, int64_t m, int64_t n, const v
 }
 
 size_t nmfb_dot_workspace_bytes(int64_t len) { return dot_workspace_bytes(len); }
+
+int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void *stream) {
+    return check(sum_parts_launch(parts, S, len, out, (cudaStream_t)stream));
+}
 
 int nmfb_dot(const void *a, int a_dtype, const void *b, int b_dtype, int64_t len, double *out,
              void *workspace, void *stream) {

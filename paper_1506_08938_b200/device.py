@@ -203,6 +203,7 @@ class Alternation:
         else:
             self.bounds_e = [0, m]
         self.qg_valid = False
+        self.index_base_e = 0  # global column of FT row 0 (multi-GPU column shards)
 
     @staticmethod
     def _splits(M, K, sms):
@@ -225,9 +226,11 @@ class Alternation:
                None, self._st())
 
     def nnls(self, side, h, h_dtype, parts, h_ld, pstride, h_base, x, count, stats):
+        # global index of problem 0: fast-break blocks are absolute (kernels.py:247)
+        base = self.index_base_e if side == 0 else 0
         L.call("nmfb_nnls_batch", self.code, self.mode, vp(self.Qa[side]), vp(self.sa[side]),
                vp(self.act[side]), vp(self.active[side]), self.r, self.r, vp(self.ra[side]),
-               vp(h), h_dtype, parts, h_ld, pstride, h_base, vp(x), count, 0,
+               vp(h), h_dtype, parts, h_ld, pstride, h_base, vp(x), count, base,
                float(self.cfg.epsilon), int(self.cfg.inner_cap), 0.0, None, None, vp(stats),
                self.lanes, self._st())
 

@@ -1,0 +1,264 @@
+"""Multi-GPU alternation: one process per GPU, columns of X / F sharded.
+
+Layout (column-sharded; north star "sharding the columns of X
+and H (and the rows of X and W for the W-update)"):
+
+* rank g owns data columns C_g (32-aligned, parallel.block_plan over
+  ranks, so fast-break blocks never straddle ranks and the per-column
+  solutions are identical to a single-GPU run) and the matching rows of F^T;
+* every rank holds all of G (n x r) for its G^T X_g pass, and solves the
+  component rows R_g (32-aligned row blocks) in the M-step.
+
+Collectives per outer iteration (torch.distributed; NCCL over NVLink on
+GPUs, gloo in the CPU tests):
+  allreduce   H_f = sum_g F_g F_g^T                 r x r fp64
+  reduce-scatter  Y^T = sum_g X_g F_g^T -> rows R_g  n x r (padded to P blocks)
+  allreduce   Q_g = sum_g G[R_g]^T G[R_g]            r x r fp64 (north-star Gram allreduce)
+  allgather   G rows R_g -> full G                   n x r
+  allreduce   objective pieces                       a few fp64 scalars
+The allgather is required by the column layout (the next coefficient step
+needs all of G); the north star lists only the first two.
+
+The per-rank numerics come from an *engine* (the CUDA engine below for the
+product; tests/ plug an oracle engine in to check the sharding logic on CPU
+with gloo).  The driver itself does no arithmetic beyond summing scalars.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from . import device as D
+
+BLOCK = L.FASTBREAK_BLOCK
+
+
+class ShardPlan:
+    """32-aligned column and row shards over `world` ranks (parallel.py:162-169)."""
+
+    def __init__(self, n, m, world):
+        self.n, self.m, self.world = n, m, world
+        self.cols = D.block_plan(m, world)
+        self.rows = D.block_plan(n, world)
+        while len(self.cols) < world:
+            self.cols.append((m, m))
+        while len(self.rows) < world:
+            self.rows.append((n, n))
+        # reduce-scatter needs equal chunks: pad every row block to the largest
+        self.row_chunk = max(hi - lo for lo, hi in self.rows)
+
+    def col_range(self, rank):
+        return self.cols[rank]
+
+    def row_range(self, rank):
+        return self.rows[rank]
+
+
+class DistAlternation:
+    """One rank's share of the alternation; engine does the local math."""
+
+    def __init__(self, engine, plan: ShardPlan, rank, group=None):
+        self.e = engine
+        self.plan = plan
+        self.rank = rank
+        self.group = group
+        self.world = plan.world
+        # with a process group every collective is issued (also at world 1, so a
+        # single-GPU torchrun exercises the NCCL path); without one, world must be 1
+        self.comm = dist.is_available() and dist.is_initialized()
+        if not self.comm and self.world != 1:
+            raise RuntimeError("world > 1 needs an initialised torch.distributed group")
+
+    # -- collectives -------------------------------------------------------
+    def _allreduce(self, t):
+        if self.comm:
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def _reduce_scatter_rows(self, yt_full):
+        """yt_full (n, r) partial -> this rank's rows (row_chunk, r) summed."""
+        p = self.plan
+        r = yt_full.shape[1]
+        chunk = p.row_chunk
+        if not self.comm:
+            lo, hi = p.row_range(0)
+            return yt_full[lo:hi]
+        padded = yt_full.new_zeros((self.world * chunk, r))
+        for g in range(self.world):
+            lo, hi = p.row_range(g)
+            padded[g * chunk: g * chunk + (hi - lo)] = yt_full[lo:hi]
+        out = yt_full.new_empty((chunk, r))
+        dist.reduce_scatter_tensor(out, padded, group=self.group)
+        lo, hi = p.row_range(self.rank)
+        return out[: hi - lo]
+
+    def _allgather_rows(self, g_rows):
+        """this rank's G rows -> full G (n, r) on every rank."""
+        p = self.plan
+        if not self.comm:
+            return g_rows
+        chunk = p.row_chunk
+        r = g_rows.shape[1]
+        send = g_rows.new_zeros((chunk, r))
+        send[: g_rows.shape[0]] = g_rows
+        recv = g_rows.new_empty((self.world * chunk, r))
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        parts = [recv[g * chunk: g * chunk + (hi - lo)] for g, (lo, hi) in enumerate(p.rows)]
+        return torch.cat(parts, 0)
+
+    # -- one outer iteration --------------------------------------------------
+    def iterate(self, k):
+        e, p = self.e, self.plan
+        rlo, rhi = p.row_range(self.rank)
+        clo, chi = p.col_range(self.rank)
+        # Gram of G: partial over my rows, allreduced (first iteration: all rows
+        # are already replicated, so every rank's partial covers its own block)
+        Qg = self._allreduce(e.gram_rows(rlo, rhi))
+        e.set_gram(Qg)
+        # coefficient step on my columns; accumulators are partial sums
+        Hf_part, yt_part = e.estep(k, clo)
+        Hf = self._allreduce(Hf_part)
+        yt_rows = self._reduce_scatter_rows(yt_part)
+        # component step on my rows
+        e.mstep(k, Hf, yt_rows, rlo, rhi)
+        G_full = self._allgather_rows(e.g_rows(rlo, rhi))
+        e.set_g(G_full)
+        # objective pieces (sum over ranks)
+        pieces = self._allreduce(e.objective_pieces(k, yt_rows, rlo, rhi))
+        e.store_pieces(k, pieces)
+
+
+# ---------------------------------------------------------------------------
+# CUDA engine: wraps device.Alternation for one rank's column block
+# ---------------------------------------------------------------------------
+class CudaEngine:
+    """Local math of one rank on its GPU (all C-ABI kernels)."""
+
+    def __init__(self, X_block, cfg, G0, FT0_block, max_iters, n_total_cols):
+        self.data = D.DeviceData(X_block, cfg.precision)
+        self.st = D.Alternation(self.data, cfg, G0, FT0_block, max_iters,
+                                precision=cfg.precision, lanes=cfg.lanes)
+        self.cfg = cfg
+        self.r = cfg.rank
+        st = self.st
+        dev = self.data.device
+        self.Qtmp = torch.zeros((self.r, self.r), dtype=torch.float64, device=dev)
+        self.Hf_part = torch.zeros_like(self.Qtmp)
+        # dense fast path: split-K partials are summed locally before the
+        # reduce-scatter; sparse / fp64: Y^T is already one fp64 buffer
+        self.ysplit = self.data.kind == "dense" and st.mode == L.MODE_FAST
+        ydt = torch.float32 if self.ysplit else st.ybuf.dtype
+        self.yt = torch.zeros((self.data.n, self.r), dtype=ydt, device=dev)
+        self.ycode = L.F32 if ydt == torch.float32 else L.F64
+        self.n_total_cols = n_total_cols
+        self.pieces = torch.zeros((12,), dtype=torch.float64, device=dev)
+
+    def gram_rows(self, lo, hi):
+        st = self.st
+        if hi > lo:
+            L.call("nmfb_gram", st.code, D.vp(st.G[lo:hi]), hi - lo, self.r, self.r,
+                   D.vp(self.Qtmp), D.vp(st.gram_ws), D.stream_handle())
+        else:
+            self.Qtmp.zero_()
+        return self.Qtmp
+
+    def set_gram(self, Q):
+        self.st.Qg.copy_(Q)
+        self.st.qg_valid = True
+
+    def estep(self, k, col_offset):
+        st = self.st
+        st.index_base_e = col_offset
+        st.estep(k)
+        # partial accumulators of my columns: H_f partial, Y^T partial (summed split-K)
+        self.Hf_part.copy_(st.Hf)
+        if self.ysplit:
+            L.call("nmfb_sum_parts", D.vp(st.ybuf), st.splits_m, self.data.n * self.r,
+                   D.vp(self.yt), D.stream_handle())
+        else:
+            self.yt.copy_(st.ybuf.view(self.data.n, self.r))
+        return self.Hf_part, self.yt
+
+    def mstep(self, k, Hf, yt_rows, lo, hi):
+        st = self.st
+        st.Hf.copy_(Hf)
+        st.rescale(st.Hf, 2.0 * self.cfg.beta2, 1)
+        if hi > lo:
+            stats = st.stats[k, 1]
+            L.call("nmfb_nnls_batch", st.code, st.mode, D.vp(st.Qa[1]), D.vp(st.sa[1]),
+                   D.vp(st.act[1]), D.vp(st.active[1]), self.r, self.r, D.vp(st.ra[1]),
+                   D.vp(yt_rows), self.ycode, 1, self.r, 0, self.cfg.beta1, D.vp(st.G[lo:hi]),
+                   hi - lo, lo, float(self.cfg.epsilon), int(self.cfg.inner_cap), 0.0, None,
+                   None, D.vp(stats), st.lanes, D.stream_handle())
+
+    def g_rows(self, lo, hi):
+        return self.st.G[lo:hi].contiguous()
+
+    def set_g(self, G_full):
+        self.st.G.copy_(G_full)
+
+    def objective_pieces(self, k, yt_rows, lo, hi):
+        """Additive per-rank pieces (slot layout of device.Alternation):
+        dense residual over my columns; sparse cross <G[R], Y^T[R]> over my
+        rows and quad <G^T G, H_f> on rank-0-equivalent terms split by rows;
+        penalty sums over my F rows and my G rows."""
+        st, cfg, d = self.st, self.cfg, self.data
+        p = self.pieces
+        p.zero_()
+        G = st.G[lo:hi]
+        if d.kind == "dense":
+            L.call("nmfb_dense_residual", st.code, D.vp(d.XT), d.m, d.n, D.vp(st.G),
+                   D.vp(st.FT), self.r, D.vp(p[0:1]), D.vp(st.res_ws), D.stream_handle())
+            if (cfg.beta1 or cfg.beta2) and hi > lo:
+                st.dot(G, st.code, None, L.F64, (hi - lo) * self.r, p[1:4])
+        else:
+            if hi > lo:
+                st.dot(G, st.code, yt_rows, self.ycode, (hi - lo) * self.r, p[1:4])
+                # quad = sum_rows-blocks <G_R^T G_R, H_f>: additive over row blocks
+                L.call("nmfb_gram", st.code, D.vp(G), hi - lo, self.r, self.r, D.vp(self.Qtmp),
+                       D.vp(st.gram_ws), D.stream_handle())
+                st.dot(self.Qtmp, L.F64, st.Hf, L.F64, self.r * self.r, p[7:10])
+        if cfg.mu1 or cfg.mu2:
+            st.dot(st.FT, st.code, None, L.F64, st.m * self.r, p[4:7])
+        return p
+
+    def store_pieces(self, k, pieces):
+        self.st.pieces[k].copy_(pieces)
+
+
+class DistFit:
+    """bench.py / users: column-sharded fit state on this rank's GPU."""
+
+    def __init__(self, X_block, cfg, init, group=None):
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        n, m_local = X_block.shape
+        m = m_local * world
+        self.plan = ShardPlan(n, m, world)
+        clo, chi = self.plan.col_range(rank)
+        if chi - clo != m_local:
+            raise ValueError("every rank must hold a 32-aligned equal column block")
+        G0, FT0 = init
+        self.engine = CudaEngine(X_block, cfg, G0, FT0, cfg.max_outer, m)
+        self.state = _StateView(DistAlternation(self.engine, self.plan, rank, group),
+                                self.engine.st)
+
+
+class _StateView:
+    """Gives bench.py the same surface as device.Alternation."""
+
+    def __init__(self, da, st):
+        self.da = da
+        self.st = st
+        self.pieces = st.pieces
+        self.splits_e = getattr(st, "splits_e", 1)
+        self.splits_m = getattr(st, "splits_m", 1)
+
+    def iterate(self, k):
+        self.da.iterate(k)
+
+    def assemble(self, *a, **kw):
+        return self.st.assemble(*a, **kw)
