@@ -202,13 +202,21 @@ def run_ours(args):
     calls = rec.summary()
     # dominant kernel: the largest share of the step
     dom = max(calls.items(), key=lambda kv: kv[1][1])
-    gemm_calls, gemm_ms = calls.get("nmfb_gemm_tall", (0, 0.0))
     hbm, peak_src = peaks()
-    # algorithmic bytes per gemm_tall launch: X once + B (K x r) + split-K partials
-    splits = (st.splits_e + st.splits_m) / 2 if hasattr(st, "splits_e") else 1
-    gemm_bytes = 4.0 * (n * m + (n + m) / 2 * RANK + splits * (n + m) / 2 * RANK)
+    gname = "nmfb_tc_gemm" if "nmfb_tc_gemm" in calls else "nmfb_gemm_tall"
+    gemm_calls, gemm_ms = calls.get(gname, (0, 0.0))
+    # algorithmic bytes per data-product launch, averaged over the two passes
+    # (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once, B^T hi+lo, split-K C
+    se, sm = getattr(st, "splits_e", 1), getattr(st, "splits_m", 1)
+    gemm_bytes = 4.0 * (n * m + RANK * (n + m) + (se * m + sm * n) * RANK / 2.0)
     gemm_avg_ms = gemm_ms / max(gemm_calls, 1)
-    achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9
+    achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9 if gemm_avg_ms > 0 else 0.0
+    kernels = {}
+    for name, (c, t) in calls.items():
+        kernels[name] = {"launches": c, "avg_ms": t / c, "share": round(t / ms, 4)}
+    if "nmfb_dense_residual_kmajor" in calls:
+        c, t = calls["nmfb_dense_residual_kmajor"]
+        kernels["nmfb_dense_residual_kmajor"]["fp32_tflops"] = 2.0 * n * m * RANK / (t / c / 1e3) / 1e12
     share = {k: round(v[1] / ms, 4) for k, v in calls.items()}
     # log sanity: objective decreasing
     pieces = st.pieces[: args.warmup + args.steps].cpu().numpy()
@@ -234,12 +242,13 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
                          % (n * m * 4 / 1e6),
                    "parallelism": f"dp{world} (column-sharded)"},
-        "roofline": {"kernel": "nmfb_gemm_tall (split-K SIMT FFMA, G^T X and X F^T passes)",
+        "roofline": {"kernel": gname + " (G^T X and X F^T passes over X; tcgen05 3xTF32)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": gemm_bytes,
                      "avg_launch_ms": gemm_avg_ms, "traffic": profile_traffic()},
         "step_share": share,
+        "kernels": kernels,
         "dominant": dom[0],
         "clocks": clk,
         "gpu_launches": rec.launches,

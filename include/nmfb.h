@@ -155,6 +155,21 @@ int nmfb_gemm_tall(const float *A, int a_kmajor, int64_t M, int64_t K, int64_t l
                    const float *B, int32_t N, int64_t ldb, float *C, int32_t splits,
                    void *stream);
 
+/* Tensor-core (tcgen05, kind::tf32, 3xTF32 split) split-K GEMM:
+ * C[s] (M x N row-major) = A(M x K, K contiguous) * Bt(N x K, K contiguous)^T
+ * over the s-th K chunk.  Bt_lo = Bt - tf32(Bt) (nmfb_split_transpose makes
+ * both from a K x N row-major B).  K % 4 == 0, N <= 160, 16-byte aligned
+ * pointers.  stages: smem pipeline depth (0 = auto).  The number of K
+ * chunks actually used is nmfb_tc_splits(K, splits). */
+int nmfb_tc_gemm(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
+                 int32_t N, float *C, int32_t splits, int32_t stages, void *stream);
+int nmfb_tc_splits(int64_t K, int32_t splits);
+/* B (K x r row-major) -> Bt_hi = B^T (r x K), Bt_lo = B^T - tf32(B^T). */
+int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, float *Bt_lo,
+                         void *stream);
+/* out (cols x rows) = in (rows x cols)^T, fp32. */
+int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream);
+
 /* Reference-order dense products (check mode), dtype F64 or F32:
  * h[col - col_lo][i] = mu1 - sum_{row, v != 0} G[row][i] * v, v = VT[col][row]
  * (kernels.py:306-313).  Cols [col_lo, col_hi). */
@@ -191,6 +206,12 @@ int nmfb_csr_yt(int dtype, int mode, const int64_t *rowptr, const int32_t *colid
 size_t nmfb_residual_workspace_bytes(int64_t m, int64_t n);
 int nmfb_dense_residual(int dtype, const void *XT, int64_t m, int64_t n, const void *G,
                         const void *FT, int32_t r, double *out, void *workspace, void *stream);
+
+/* fp32 production form: the same residual from the k-major operand copies the
+ * tensor-core passes keep, Gt = G^T (r x n) and Ft = F (r x m); XT (m x n). */
+int nmfb_dense_residual_kmajor(const float *XT, int64_t m, int64_t n, const float *Gt,
+                               const float *Ft, int32_t r, double *out, void *workspace,
+                               void *stream);
 
 /* out[i] = sum_{s < S} parts[s * len + i], fixed order (split-K partials of
  * X F^T summed before the multi-GPU reduce-scatter).  float32. */

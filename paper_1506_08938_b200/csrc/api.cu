@@ -37,6 +37,14 @@ int dot_launch(const void *a, int a_dtype, const void *b, int b_dtype, int64_t l
 int add_into_launch(int dtype, void *dst, const void *src, int64_t len, int upper_r,
                     cudaStream_t st);
 int sum_parts_launch(const float *parts, int S, int64_t len, float *out, cudaStream_t st);
+int dense_residual_kmajor_launch(const float *XT, int64_t m, int64_t n, const float *Gt,
+                                 const float *Ft, int r, double *out, void *ws, cudaStream_t st);
+int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
+                   int N, float *C, int splits, int stages, cudaStream_t st);
+int tc_effective_splits(int64_t K, int splits);
+int split_transpose_launch(const float *B, int64_t K, int r, float *hi, float *lo,
+                           cudaStream_t st);
+int transpose_launch(const float *in, int64_t rows, int64_t cols, float *out, cudaStream_t st);
 int csc_scatter_yt_launch(int dtype, const int64_t *indptr, const int32_t *rowidx,
                           const void *vals, int64_t lo, int64_t hi, const void *FT, int r,
                           void *YT, cudaStream_t st);
@@ -208,10 +216,34 @@ int nmfb_dense_residual(int dtype, const void *XT, int64_t m, int64_t n, const v
                                        (cudaStream_t)stream));
 }
 
+int nmfb_dense_residual_kmajor(const float *XT, int64_t m, int64_t n, const float *Gt,
+                               const float *Ft, int32_t r, double *out, void *workspace,
+                               void *stream) {
+    return check(dense_residual_kmajor_launch(XT, m, n, Gt, Ft, r, out, workspace,
+                                              (cudaStream_t)stream));
+}
+
 size_t nmfb_dot_workspace_bytes(int64_t len) { return dot_workspace_bytes(len); }
 
 int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void *stream) {
     return check(sum_parts_launch(parts, S, len, out, (cudaStream_t)stream));
+}
+
+int nmfb_tc_gemm(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
+                 int32_t N, float *C, int32_t splits, int32_t stages, void *stream) {
+    return check(tc_gemm_launch(A, M, K, Bt_hi, Bt_lo, N, C, splits, stages,
+                                (cudaStream_t)stream));
+}
+
+int nmfb_tc_splits(int64_t K, int32_t splits) { return tc_effective_splits(K, splits); }
+
+int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, float *Bt_lo,
+                         void *stream) {
+    return check(split_transpose_launch(B, K, r, Bt_hi, Bt_lo, (cudaStream_t)stream));
+}
+
+int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream) {
+    return check(transpose_launch(in, rows, cols, out, (cudaStream_t)stream));
 }
 
 int nmfb_dot(const void *a, int a_dtype, const void *b, int b_dtype, int64_t len, double *out,

@@ -374,6 +374,94 @@ __global__ void __launch_bounds__(256) residual_kernel(const T *__restrict__ XT,
     if (tid == 0) part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = red[0];
 }
 
+// fp32 production residual: CTA tile 128 (m, columns of X) x 128 (n, rows of
+// X), 256 threads with an 8x8 register block each, K = r staged through
+// shared memory 32 at a time ([k][j] layouts -> float4 reads).  FFMA-bound:
+// 2*n*m*r flops; the residual itself is formed and squared in fp32
+// (round-to-nearest, unbiased) and summed in fp64 per CTA.
+constexpr int R2T = 128, R2K = 32;
+
+// Operands are the k-major copies the tensor-core passes already keep:
+// Gt (r x n) = G^T and Ft (r x m) = F, so every smem fill is a coalesced,
+// bank-conflict-free row copy.
+__global__ void __launch_bounds__(256, 2) residual_f32_kernel(const float *__restrict__ XT,
+                                                              int64_t m, int64_t n,
+                                                              const float *__restrict__ Gt,
+                                                              const float *__restrict__ Ft,
+                                                              int r, double *__restrict__ part) {
+    __shared__ __align__(16) float Fs[R2K][R2T];
+    __shared__ __align__(16) float Gs[R2K][R2T];
+    __shared__ double red[8];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t j0 = (int64_t)blockIdx.y * R2T;  // m
+    const int64_t r0 = (int64_t)blockIdx.x * R2T;  // n
+    float acc[8][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = 0.f;
+    for (int kb = 0; kb < r; kb += R2K) {
+        for (int idx = tid; idx < R2K * R2T; idx += 256) {
+            const int kk = idx / R2T, t = idx % R2T;
+            const int gk = kb + kk;
+            const int64_t gj = j0 + t, gr = r0 + t;
+            Fs[kk][t] = (gj < m && gk < r) ? Ft[(int64_t)gk * m + gj] : 0.f;
+            Gs[kk][t] = (gr < n && gk < r) ? Gt[(int64_t)gk * n + gr] : 0.f;
+        }
+        __syncthreads();
+        const int kmax = min(R2K, r - kb);
+        for (int kk = 0; kk < kmax; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(&Fs[kk][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&Fs[kk][ty * 8 + 4]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Gs[kk][tx * 8]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Gs[kk][tx * 8 + 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+    double s = 0.0;
+    const bool vec = (n % 4 == 0) && (r0 + tx * 8 + 7 < n);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int64_t gj = j0 + ty * 8 + u;
+        if (gj >= m) continue;
+        const float *xrow = XT + gj * n + r0 + tx * 8;
+        float x[8];
+        if (vec) {
+            const float4 x0 = *reinterpret_cast<const float4 *>(xrow);
+            const float4 x1 = *reinterpret_cast<const float4 *>(xrow + 4);
+            x[0] = x0.x; x[1] = x0.y; x[2] = x0.z; x[3] = x0.w;
+            x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
+        } else {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) x[v] = (r0 + tx * 8 + v < n) ? xrow[v] : 0.f;
+        }
+        float su = 0.f;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+            if (r0 + tx * 8 + v < n) {
+                const float d = x[v] - acc[u][v];
+                su = fmaf(d, d, su);
+            }
+        }
+        s += (double)su;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(NMFB_FULL_MASK, s, o);
+    if ((tid & 31) == 0) red[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        part[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 __global__ void sum_parts_kernel(const double *__restrict__ part, int64_t np, double scale,
                                  double *__restrict__ out) {
     __shared__ double red[256];
@@ -390,16 +478,17 @@ __global__ void sum_parts_kernel(const double *__restrict__ part, int64_t np, do
 }
 
 size_t residual_workspace_bytes(int64_t m, int64_t n) {
+    // sized for the smaller (fp64) tile, which has the most CTAs
     return (size_t)((m + RT - 1) / RT) * (size_t)((n + RT - 1) / RT) * sizeof(double);
 }
 
 int dense_residual_launch(int dtype, const void *XT, int64_t m, int64_t n, const void *G,
                           const void *FT, int r, double *out, void *ws, cudaStream_t st) {
     if (m <= 0 || n <= 0) return NMFB_OK;
+    double *part = (double *)ws;
     int64_t gx = (n + RT - 1) / RT, gy = (m + RT - 1) / RT;
     if (gy > 65535) return NMFB_ERR_ARG;
     dim3 grid((unsigned)gx, (unsigned)gy);
-    double *part = (double *)ws;
     if (dtype == NMFB_F64)
         residual_kernel<double><<<grid, 256, 0, st>>>((const double *)XT, m, n,
                                                       (const double *)G, (const double *)FT, r,
@@ -407,6 +496,19 @@ int dense_residual_launch(int dtype, const void *XT, int64_t m, int64_t n, const
     else
         residual_kernel<float><<<grid, 256, 0, st>>>((const float *)XT, m, n, (const float *)G,
                                                      (const float *)FT, r, part);
+    sum_parts_kernel<<<1, 256, 0, st>>>(part, gx * gy, 0.5, out);
+    return launch_status();
+}
+
+int dense_residual_kmajor_launch(const float *XT, int64_t m, int64_t n, const float *Gt,
+                                 const float *Ft, int r, double *out, void *ws,
+                                 cudaStream_t st) {
+    if (m <= 0 || n <= 0) return NMFB_OK;
+    double *part = (double *)ws;
+    int64_t gx = (n + R2T - 1) / R2T, gy = (m + R2T - 1) / R2T;
+    if (gy > 65535) return NMFB_ERR_ARG;
+    residual_f32_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, st>>>(XT, m, n, Gt, Ft, r,
+                                                                          part);
     sum_parts_kernel<<<1, 256, 0, st>>>(part, gx * gy, 0.5, out);
     return launch_status();
 }

@@ -36,6 +36,13 @@ _TORCH = {"fp32": torch.float32, "fp64": torch.float64}
 _CODE = {"fp32": L.F32, "fp64": L.F64}
 
 
+def tc_enabled():
+    """Tensor-core passes on unless NMFB_DISABLE_TC=1 (A/B comparisons only)."""
+    import os
+
+    return os.environ.get("NMFB_DISABLE_TC", "0") != "1"
+
+
 def require_cuda():
     L.lib()
     if not torch.cuda.is_available():
@@ -132,6 +139,14 @@ class DeviceData:
             self.XT = torch.from_numpy(xt).to(self.device)
             self.host = None
 
+    def ensure_x_rowmajor(self):
+        """X (n, m) row-major next to X^T: the K-major operand of the Y^T pass
+        (one transpose kernel per fit; HBM is plentiful, TMA wants K-major)."""
+        if getattr(self, "X", None) is None:
+            self.X = torch.empty((self.n, self.m), dtype=self.XT.dtype, device=self.XT.device)
+            L.call("nmfb_transpose", vp(self.XT), self.m, self.n, vp(self.X), stream_handle())
+        return self.X
+
     @classmethod
     def from_device_dense(cls, XT, precision):
         """Wrap an existing (m, n) device tensor (already in HBM)."""
@@ -183,10 +198,21 @@ class Alternation:
         if data.kind == "dense":
             self.res_ws = torch.empty((L.lib().nmfb_residual_workspace_bytes(m, n) // 8 + 1,),
                                       dtype=f64, device=dev)
+        # tensor-core passes (tcgen05 3xTF32) when the shapes allow TMA tiles:
+        # both orientations of X resident (X^T for G^T X, X for X F^T)
+        self.use_tc = (data.kind == "dense" and self.mode == L.MODE_FAST and r <= 160
+                       and n % 4 == 0 and m % 4 == 0 and tc_enabled())
         if data.kind == "dense" and self.mode == L.MODE_FAST:
-            # split-K factors: ~4 CTAs per SM for each pass
-            self.splits_e = splits or self._splits(m, n, sms)
-            self.splits_m = splits or self._splits(n, m, sms)
+            if self.use_tc:
+                data.ensure_x_rowmajor()
+                self.splits_e = splits or L.lib().nmfb_tc_splits(n, self._tc_splits(m, sms))
+                self.splits_m = splits or L.lib().nmfb_tc_splits(m, self._tc_splits(n, sms))
+                self.Gt = torch.empty((2, r, n), dtype=torch.float32, device=dev)
+                self.Ft = torch.empty((2, r, m), dtype=torch.float32, device=dev)
+            else:
+                # split-K factors: ~4 CTAs per SM for each pass
+                self.splits_e = splits or self._splits(m, n, sms)
+                self.splits_m = splits or self._splits(n, m, sms)
             self.hbuf = torch.empty((self.splits_e * m * r,), dtype=torch.float32, device=dev)
             self.ybuf = torch.empty((self.splits_m * n * r,), dtype=torch.float32, device=dev)
         else:
@@ -204,6 +230,13 @@ class Alternation:
             self.bounds_e = [0, m]
         self.qg_valid = False
         self.index_base_e = 0  # global column of FT row 0 (multi-GPU column shards)
+        self.gt_valid = False  # Gt holds tf32-split G^T of the current G
+
+    @staticmethod
+    def _tc_splits(M, sms):
+        # one 128-row tile per CTA, 1 CTA/SM: ~8 waves keeps the tail short
+        tiles = -(-M // 128)
+        return int(max(1, min(16, round(8 * sms / tiles))))
 
     @staticmethod
     def _splits(M, K, sms):
@@ -250,7 +283,15 @@ class Alternation:
         self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
         st = self.stats[k, 0]
         if d.kind == "dense":
-            if self.mode == L.MODE_FAST:
+            if self.use_tc:
+                if not self.gt_valid:
+                    L.call("nmfb_split_transpose", vp(self.G), n, r, vp(self.Gt[0]),
+                           vp(self.Gt[1]), self._st())
+                self.gt_valid = False
+                L.call("nmfb_tc_gemm", vp(d.XT), m, n, vp(self.Gt[0]), vp(self.Gt[1]), r,
+                       vp(self.hbuf), self.splits_e, 0, self._st())
+                self.nnls(0, self.hbuf, L.F32, self.splits_e, r, m * r, cfg.mu1, self.FT, m, st)
+            elif self.mode == L.MODE_FAST:
                 L.call("nmfb_gemm_tall", vp(d.XT), 1, m, n, n, vp(self.G), r, r, vp(self.hbuf),
                        self.splits_e, self._st())
                 self.nnls(0, self.hbuf, L.F32, self.splits_e, r, m * r, cfg.mu1, self.FT, m, st)
@@ -270,7 +311,12 @@ class Alternation:
         else:
             self.gram(self.FT, m, self.Hf)
         if d.kind == "dense":
-            if self.mode == L.MODE_FAST:
+            if self.use_tc:
+                L.call("nmfb_split_transpose", vp(self.FT), m, r, vp(self.Ft[0]), vp(self.Ft[1]),
+                       self._st())
+                L.call("nmfb_tc_gemm", vp(d.X), n, m, vp(self.Ft[0]), vp(self.Ft[1]), r,
+                       vp(self.ybuf), self.splits_m, 0, self._st())
+            elif self.mode == L.MODE_FAST:
                 L.call("nmfb_gemm_tall", vp(d.XT), 0, n, m, n, vp(self.FT), r, r,
                        vp(self.ybuf), self.splits_m, self._st())
             else:
@@ -299,7 +345,15 @@ class Alternation:
         """Objective pieces of iteration k into self.pieces[k] (nmf.py:152-165)."""
         cfg, d = self.cfg, self.d
         p = self.pieces[k]
-        if d.kind == "dense":
+        if d.kind == "dense" and self.use_tc:
+            # k-major G^T for the residual, reused by the next coefficient step;
+            # F = Ft[0] is current (made by this iteration's Y^T pass)
+            L.call("nmfb_split_transpose", vp(self.G), self.n, self.r, vp(self.Gt[0]),
+                   vp(self.Gt[1]), self._st())
+            self.gt_valid = True
+            L.call("nmfb_dense_residual_kmajor", vp(d.XT), self.m, self.n, vp(self.Gt[0]),
+                   vp(self.Ft[0]), self.r, vp(p[0:1]), vp(self.res_ws), self._st())
+        elif d.kind == "dense":
             # 0.5 ||X - G F||^2 by tile residual; G F never stored
             L.call("nmfb_dense_residual", self.code, vp(d.XT), self.m, self.n, vp(self.G),
                    vp(self.FT), self.r, vp(p[0:1]), vp(self.res_ws), self._st())
