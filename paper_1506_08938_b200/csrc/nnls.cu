@@ -37,7 +37,7 @@ static int launch_fast(const NnlsLaunch &p) {
     // with a device-side ra the variant must cover the full rank r
     const int need = p.ra_dev ? p.r : p.ra;
     int L = p.lanes;
-    if (L == 0) L = need <= 16 ? 1 : (need <= 64 ? 2 : (need <= 128 ? 4 : 8));
+    if (L == 0) L = need <= 16 ? 1 : (need <= 56 ? 8 : (need <= 128 ? 8 : 8));
     const bool h64 = p.h_dtype == NMFB_F64;
     int E;
     switch (L) {

@@ -42,14 +42,51 @@ __device__ __forceinline__ void q_times(float (&acc)[E], const float (&src)[E], 
     }
 }
 
-// Occupancy target: ~6E + 64 live registers per thread (y, grad, Qd, d and
-// line-search temporaries per coordinate) -> resident CTAs per SM.
-constexpr int nnls_min_blocks(int E, int threads) {
-    return (65536 / ((6 * E + 64) * threads)) < 1 ? 1 : (65536 / ((6 * E + 64) * threads));
+// h = h_base - sum of the split-K partials, with independent loads in flight
+// (four accumulators) instead of a load -> add dependency chain.
+template <typename TH>
+__device__ __forceinline__ float fast_h(const NnlsArgs<float, TH> &a, int64_t j, int i) {
+    const TH *p = a.hp + j * a.h_ld + i;
+    if (a.S == 0) return (float)p[0];
+    TH s0 = p[0], s1 = TH(0), s2 = TH(0), s3 = TH(0);
+    int k = 1;
+    for (; k + 3 < a.S; k += 4) {
+        s0 += p[(int64_t)k * a.h_pstride];
+        s1 += p[(int64_t)(k + 1) * a.h_pstride];
+        s2 += p[(int64_t)(k + 2) * a.h_pstride];
+        s3 += p[(int64_t)(k + 3) * a.h_pstride];
+    }
+    for (; k < a.S; ++k) s0 += p[(int64_t)k * a.h_pstride];
+    return (float)((TH)a.h_base - ((s0 + s1) + (s2 + s3)));
+}
+
+// Same, with the source values produced by a functor of the element index
+// (recomputed instead of held in registers: d = passive gradient, delta = step).
+template <int E, int L, typename F>
+__device__ __forceinline__ void q_times_f(float (&acc)[E], F src, const float *Qrow, int S,
+                                          unsigned gmask) {
+#pragma unroll 1
+    for (int jl = 0; jl < L; ++jl) {
+#pragma unroll
+        for (int je = 0; je < E; ++je) {
+            const float mine = src(je);
+            const float sj = (L == 1) ? mine : __shfl_sync(gmask, mine, jl, L);
+            const int jcol = je * L + jl;
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[e] = fmaf(Qrow[e * L * S + jcol], sj, acc[e]);
+        }
+    }
+}
+
+// Occupancy target: ~4E + 48 live registers per thread (y, grad and Q*d per
+// coordinate; the passive gradient and step are recomputed) -> CTAs per SM.
+__host__ __device__ constexpr int nnls_regs(int E, int L) { return 4 * E + 48 + (L == 1 ? 48 : 0); }
+__host__ __device__ constexpr int nnls_min_blocks(int E, int L, int threads) {
+    return (65536 / (nnls_regs(E, L) * threads)) < 1 ? 1 : (65536 / (nnls_regs(E, L) * threads));
 }
 
 template <typename TH, int E, int L, int B>
-__global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
+__global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     nnls_fast_kernel(NnlsArgs<float, TH> a) {
     constexpr int R = E * L;
     constexpr int S = R | 1;
@@ -82,7 +119,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
     const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
     const float *Qrow = Qs + l * S;  // row of coordinate e is Qrow + e*L*S
 
-    float y[E], gr[E], qd[E], dv[E];
+    float y[E], gr[E], qd[E];
 
     int status = ST_DONE;
     bool fail = false, write_x = false;
@@ -90,16 +127,22 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
     float final_norm = 0.f, norm_k = 0.f, threshold = 0.f;
 
     // ---- prologue: short-circuit, frozen check, compact load, gradient ----
+    // The problem's full linear term h (sum of the split-K partials, loads
+    // issued 4 at a time) is staged once in shared memory: the short-circuit
+    // scan and the compact gather h[act_idx[k]] both read it from there.
+    float *hrow = smem_f + R * S + (size_t)slot * r;
     bool any_neg = false, frozen_neg = false;
     if (valid) {
         for (int i = l; i < r; i += L) {
-            float hv = load_h<float, TH, Fast<float>>(a, j, i);
+            const float hv = fast_h<TH>(a, j, i);
+            hrow[i] = hv;
             if (hv < 0.f) {
                 any_neg = true;
                 if (!a.active[i]) frozen_neg = true;
             }
         }
     }
+    __syncwarp(gmask);
     any_neg = gany<L>(any_neg, gmask, gbase);
     frozen_neg = gany<L>(frozen_neg, gmask, gbase);
     if (valid) {
@@ -117,7 +160,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
         if (solve && k < ra) {
             const int ik = a.act_idx[k];
             const float sv = a.scale_a[k];
-            qv = __fdiv_rn(load_h<float, TH, Fast<float>>(a, j, ik), sv);
+            qv = __fdiv_rn(hrow[ik], sv);
             yv = a.x[j * r + ik] * sv;
         }
         y[e] = yv;
@@ -139,58 +182,62 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
     }
 
     // ---- lockstep iterations with per-block fast-break resolution ----
+    // passive-set gradient component (kernels.py:59-64): g if y > 0 or g < 0
+    auto pgrad = [](float yv, float gv) { return (yv > 0.f || gv < 0.f) ? gv : 0.f; };
     while (true) {
         if (status == ST_RUNNING) {
             bool moved = false;
+            // exact line search over the passive set (kernels.py:57-103)
             float nsq = 0.f;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                dv[e] = (y[e] > 0.f || gr[e] < 0.f) ? gr[e] : 0.f;
-                nsq = fmaf(dv[e], dv[e], nsq);
+                const float d = pgrad(y[e], gr[e]);
+                nsq = fmaf(d, d, nsq);
             }
             nsq = gsum<L>(nsq, gmask);
             if (nsq > 0.f) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) qd[e] = 0.f;
-                q_times<E, L>(qd, dv, Qrow, S, gmask);
+                q_times_f<E, L>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qrow, S, gmask);
                 float curv = 0.f;
 #pragma unroll
-                for (int e = 0; e < E; ++e) curv = fmaf(dv[e], qd[e], curv);
+                for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
                 curv = gsum<L>(curv, gmask);
                 const float alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
                 bool clamped = false;
 #pragma unroll
                 for (int e = 0; e < E; ++e)
-                    if (fmaf(-alpha, dv[e], y[e]) < 0.f) clamped = true;
+                    if (fmaf(-alpha, pgrad(y[e], gr[e]), y[e]) < 0.f) clamped = true;
                 clamped = gany<L>(clamped, gmask, gbase);
-                float step = alpha;
                 if (clamped) {
-                    float delta[E];
+                    // _take_step (kernels.py:153-175) with the breakpoint fallback
+                    float step = alpha;
                     for (int pass = 0; pass < 2; ++pass) {
+                        auto delta = [&](int e) {
+                            return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
+                        };
 #pragma unroll
-                        for (int e = 0; e < E; ++e) {
-                            delta[e] = fmaxf(fmaf(-step, dv[e], y[e]), 0.f) - y[e];
-                            qd[e] = 0.f;
-                        }
-                        q_times<E, L>(qd, delta, Qrow, S, gmask);
+                        for (int e = 0; e < E; ++e) qd[e] = 0.f;
+                        q_times_f<E, L>(qd, delta, Qrow, S, gmask);
                         if (pass == 1) break;
                         float df = 0.f;
 #pragma unroll
-                        for (int e = 0; e < E; ++e)
-                            df += gr[e] * delta[e] + 0.5f * delta[e] * qd[e];
+                        for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
                         df = gsum<L>(df, gmask);
                         if (!(df > 0.f)) break;
                         float abp = INFINITY;
 #pragma unroll
-                        for (int e = 0; e < E; ++e)
-                            if (dv[e] > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], dv[e]));
+                        for (int e = 0; e < E; ++e) {
+                            const float d = pgrad(y[e], gr[e]);
+                            if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                        }
                         abp = gmin<L>(abp, gmask);
                         if (!(abp < alpha)) break;
                         step = abp;
                     }
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
-                        float v = fmaxf(fmaf(-step, dv[e], y[e]), 0.f);
+                        const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
                         if (v != y[e]) moved = true;
                         y[e] = v;
                         gr[e] += qd[e];
@@ -198,14 +245,17 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
                 } else {
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
-                        float v = fmaf(-alpha, dv[e], y[e]);
+                        const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
                         if (v != y[e]) moved = true;
                         y[e] = v;
                         gr[e] = fmaf(-alpha, qd[e], gr[e]);
                     }
                 }
             }
-            // greedy coordinate descent: r selections, pending update fused
+            // greedy coordinate descent: ra selections, the chosen coordinate's
+            // gradient column update fused into the next scan (kernels.py:104-132).
+            // Closed-form step dx = max(y - g, 0) - y = -min(g, y); decrease
+            // |g dx + dx^2 / 2| = |dx (g + dx / 2)|; ties -> lowest index.
             int pp = -1;
             float pdx = 0.f;
             for (int s = 0; s < ra; ++s) {
@@ -220,24 +270,28 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, 32 * L * B))
                         gr[e] = gi;
                         if (k == pp) y[e] += pdx;
                     }
-                    float dxi = fmaxf(y[e] - gi, 0.f) - y[e];
-                    float dec = fabsf(gi * dxi + 0.5f * dxi * dxi);
+                    const float dxi = -fminf(gi, y[e]);
+                    const float dec = fabsf(dxi * fmaf(0.5f, dxi, gi));
                     if (dec > best) {
                         best = dec;
                         bp = k;
                         bdx = dxi;
                     }
                 }
+                if (L > 1) {
+                    const int mine = bp;
 #pragma unroll
-                for (int o = L / 2; o > 0; o >>= 1) {
-                    float ob = __shfl_xor_sync(gmask, best, o, L);
-                    int op = __shfl_xor_sync(gmask, bp, o, L);
-                    float od = __shfl_xor_sync(gmask, bdx, o, L);
-                    if (ob > best || (ob == best && op < bp)) {
-                        best = ob;
-                        bp = op;
-                        bdx = od;
+                    for (int o = L / 2; o > 0; o >>= 1) {
+                        const float ob = __shfl_xor_sync(gmask, best, o, L);
+                        const int op = __shfl_xor_sync(gmask, bp, o, L);
+                        if (ob > best || (ob == best && op < bp)) {
+                            best = ob;
+                            bp = op;
+                        }
                     }
+                    // step of the winner, broadcast from the lane that owns it
+                    const float wdx = (bp == mine) ? bdx : 0.f;
+                    bdx = __shfl_sync(gmask, wdx, (bp == INT_MAX) ? 0 : (bp % L), L);
                 }
                 if (!(best > 0.f)) {
                     pp = -1;
@@ -337,7 +391,8 @@ template <typename TH, int E, int L, int B>
 static int launch_fast_variant(const NnlsLaunch &p) {
     auto a = make_args<float, TH>(p);
     constexpr int R = E * L, S = R | 1;
-    size_t smem = sizeof(float) * R * S;
+    // Q (R x S) + one staged h row (r floats) per problem slot
+    size_t smem = sizeof(float) * ((size_t)R * S + (size_t)32 * B * p.r);
     auto kern = nnls_fast_kernel<TH, E, L, B>;
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

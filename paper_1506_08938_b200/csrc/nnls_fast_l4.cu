@@ -4,7 +4,7 @@
 
 namespace nmfb {
 
-#define NMFB_VARIANTS_L4(X) X(16, 4, 2) X(25, 4, 2) X(32, 4, 2)
+#define NMFB_VARIANTS_L4(X) X(13, 4, 2) X(16, 4, 2) X(25, 4, 2) X(32, 4, 2)
 
 // smallest E with E * 4 >= need; returns E or 0
 int fast_pick_l4(int need) {

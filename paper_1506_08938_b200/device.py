@@ -207,8 +207,15 @@ class Alternation:
                 data.ensure_x_rowmajor()
                 self.splits_e = splits or L.lib().nmfb_tc_splits(n, self._tc_splits(m, sms))
                 self.splits_m = splits or L.lib().nmfb_tc_splits(m, self._tc_splits(n, sms))
-                self.Gt = torch.empty((2, r, n), dtype=torch.float32, device=dev)
-                self.Ft = torch.empty((2, r, m), dtype=torch.float32, device=dev)
+                # [iteration parity][hi, lo] k-major tf32 splits of G^T and F; two
+                # parities so the residual of iteration k (side stream) can still
+                # read its operands while iteration k+1 runs
+                self.Gt = torch.empty((2, 2, r, n), dtype=torch.float32, device=dev)
+                self.Ft = torch.empty((2, 2, r, m), dtype=torch.float32, device=dev)
+                lo, hi = torch.cuda.Stream.priority_range()
+                self.main = torch.cuda.Stream(device=dev, priority=hi)
+                self.side = torch.cuda.Stream(device=dev, priority=lo)
+                self.res_ev = [None, None]
             else:
                 # split-K factors: ~4 CTAs per SM for each pass
                 self.splits_e = splits or self._splits(m, n, sms)
@@ -284,11 +291,14 @@ class Alternation:
         st = self.stats[k, 0]
         if d.kind == "dense":
             if self.use_tc:
+                gq = (k - 1) % 2  # parity buffer holding G_{k-1}^T
+                Gt = self.Gt[gq]
                 if not self.gt_valid:
-                    L.call("nmfb_split_transpose", vp(self.G), n, r, vp(self.Gt[0]),
-                           vp(self.Gt[1]), self._st())
+                    self._wait_residual(gq)
+                    L.call("nmfb_split_transpose", vp(self.G), n, r, vp(Gt[0]), vp(Gt[1]),
+                           self._st())
                 self.gt_valid = False
-                L.call("nmfb_tc_gemm", vp(d.XT), m, n, vp(self.Gt[0]), vp(self.Gt[1]), r,
+                L.call("nmfb_tc_gemm", vp(d.XT), m, n, vp(Gt[0]), vp(Gt[1]), r,
                        vp(self.hbuf), self.splits_e, 0, self._st())
                 self.nnls(0, self.hbuf, L.F32, self.splits_e, r, m * r, cfg.mu1, self.FT, m, st)
             elif self.mode == L.MODE_FAST:
@@ -312,9 +322,11 @@ class Alternation:
             self.gram(self.FT, m, self.Hf)
         if d.kind == "dense":
             if self.use_tc:
-                L.call("nmfb_split_transpose", vp(self.FT), m, r, vp(self.Ft[0]), vp(self.Ft[1]),
+                Ft = self.Ft[k % 2]
+                self._wait_residual(k % 2)  # residual(k-2) still reads this parity
+                L.call("nmfb_split_transpose", vp(self.FT), m, r, vp(Ft[0]), vp(Ft[1]),
                        self._st())
-                L.call("nmfb_tc_gemm", vp(d.X), n, m, vp(self.Ft[0]), vp(self.Ft[1]), r,
+                L.call("nmfb_tc_gemm", vp(d.X), n, m, vp(Ft[0]), vp(Ft[1]), r,
                        vp(self.ybuf), self.splits_m, 0, self._st())
             elif self.mode == L.MODE_FAST:
                 L.call("nmfb_gemm_tall", vp(d.XT), 0, n, m, n, vp(self.FT), r, r,
@@ -348,11 +360,22 @@ class Alternation:
         if d.kind == "dense" and self.use_tc:
             # k-major G^T for the residual, reused by the next coefficient step;
             # F = Ft[0] is current (made by this iteration's Y^T pass)
-            L.call("nmfb_split_transpose", vp(self.G), self.n, self.r, vp(self.Gt[0]),
-                   vp(self.Gt[1]), self._st())
+            q = k % 2
+            Gt, Ft = self.Gt[q], self.Ft[q]
+            L.call("nmfb_split_transpose", vp(self.G), self.n, self.r, vp(Gt[0]), vp(Gt[1]),
+                   self._st())
             self.gt_valid = True
-            L.call("nmfb_dense_residual_kmajor", vp(d.XT), self.m, self.n, vp(self.Gt[0]),
-                   vp(self.Ft[0]), self.r, vp(p[0:1]), vp(self.res_ws), self._st())
+            # the FFMA-bound residual runs on a side stream, overlapping the next
+            # iteration's HBM/smem-bound tensor-core pass and latency-bound NNLS
+            ready = torch.cuda.Event()
+            ready.record()
+            self.side.wait_event(ready)
+            with torch.cuda.stream(self.side):
+                L.call("nmfb_dense_residual_kmajor", vp(d.XT), self.m, self.n, vp(Gt[0]),
+                       vp(Ft[0]), self.r, vp(p[0:1]), vp(self.res_ws), stream_handle(self.side))
+                ev = torch.cuda.Event()
+                ev.record(self.side)
+            self.res_ev[q] = ev
         elif d.kind == "dense":
             # 0.5 ||X - G F||^2 by tile residual; G F never stored
             L.call("nmfb_dense_residual", self.code, vp(d.XT), self.m, self.n, vp(self.G),
@@ -369,10 +392,37 @@ class Alternation:
         if (cfg.beta1 or cfg.beta2) and d.kind == "dense":
             self.dot(self.G, self.code, None, L.F64, self.n * self.r, p[1:4])
 
+    def _wait_residual(self, q):
+        """Main stream waits until the side-stream residual reading parity q is done."""
+        ev = self.res_ev[q] if self.use_tc else None
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+            self.res_ev[q] = None
+
+    def join(self):
+        """Make the caller's stream wait for all work of this state (the
+        high-priority main stream and the side-stream objective)."""
+        main = getattr(self, "main", None)
+        if main is not None:
+            with torch.cuda.stream(main):
+                for q in (0, 1):
+                    self._wait_residual(q)
+            torch.cuda.current_stream().wait_stream(main)
+
     def iterate(self, k):
-        self.estep(k)
-        self.mstep(k)
-        self.objective(k)
+        main = getattr(self, "main", None)
+        if main is None:
+            self.estep(k)
+            self.mstep(k)
+            self.objective(k)
+            return
+        # the step runs on a high-priority stream so the FFMA-bound residual on
+        # the low-priority side stream only fills SM slots the step leaves idle
+        main.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(main):
+            self.estep(k)
+            self.mstep(k)
+            self.objective(k)
 
     # -- host views ------------------------------------------------------------
     @staticmethod

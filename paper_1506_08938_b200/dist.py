@@ -260,5 +260,8 @@ class _StateView:
     def iterate(self, k):
         self.da.iterate(k)
 
+    def join(self):
+        self.st.join()
+
     def assemble(self, *a, **kw):
         return self.st.assemble(*a, **kw)

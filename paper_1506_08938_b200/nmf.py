@@ -224,6 +224,8 @@ class FitSession:
         try:
             for k in range(cfg.max_outer):
                 st.iterate(k)
+                if sync_each or k == cfg.max_outer - 1:
+                    st.join()
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record()
                 events.append(ev)
@@ -246,6 +248,7 @@ class FitSession:
                         break
                     previous = obj
             if not sync_each:
+                st.join()
                 events[-1].synchronize()
                 stats = st.stats[:done].cpu().numpy()
                 pieces = st.pieces[:done].cpu().numpy()
