@@ -200,6 +200,16 @@ int nmfb_csr_yt(int dtype, int mode, const int64_t *rowptr, const int32_t *colid
                 const void *vals, int64_t n, const void *FT, int32_t r, int yt_dtype,
                 const int64_t *shard_bounds, int32_t workers, void *YT, void *stream);
 
+/* Load-balanced production form of the Y^T pass (fast mode): rows cut into
+ * chunks of bounded length (a plan built once per matrix, see
+ * paper_1506_08938_b200/device.py csr_chunk_plan).  chunks: int64
+ * [nchunks][4] = (row, lo, hi, slot) with slot -1 for single-chunk rows;
+ * heavy: int64 [nheavy][3] = (row, first slot, count); part: workspace of
+ * (total slots) x r elements of yt_dtype.  Deterministic. */
+int nmfb_csr_yt_chunked(int dtype, const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                        int64_t nheavy, const int32_t *colidx, const void *vals, const void *FT,
+                        int32_t r, int yt_dtype, void *YT, void *part, void *stream);
+
 /* Dense residual 0.5 * ||X - G F||^2 with X given as XT (m, n) row-major,
  * G (n, r), FT (m, r); fp64 accumulation; result added to *out (device
  * double) deterministically.  workspace: nmfb_residual_workspace_bytes. */

@@ -65,6 +65,8 @@ SIGNATURES = {
     "nmfb_csc_linear": (_int, [_int, _int, _vp, _vp, _vp, _i64, _i64, _vp, _i32, _f64, _vp, _vp]),
     "nmfb_csr_yt": (_int, [_int, _int, _vp, _vp, _vp, _i64, _vp, _i32, _int, _pi64, _i32, _vp,
                            _vp]),
+    "nmfb_csr_yt_chunked": (_int, [_int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i32, _int, _vp,
+                                   _vp, _vp]),
     "nmfb_residual_workspace_bytes": (_sz, [_i64, _i64]),
     "nmfb_dense_residual": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
     "nmfb_dense_residual_kmajor": (_int, [_vp, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
@@ -120,7 +122,7 @@ KERNELS_PER_CALL = {
     "nmfb_nnls_batch": 1, "nmfb_nqp_solve": 1, "nmfb_gram": 2, "nmfb_rescale": 1,
     "nmfb_gemm_tall": 1, "nmfb_dense_linear_ref": 1, "nmfb_dense_yt_ref": 1, "nmfb_hp_ref": 1,
     "nmfb_csc_linear": 1, "nmfb_csr_yt": 1, "nmfb_dense_residual": 2, "nmfb_dot": 2,
-    "nmfb_sum_parts": 1, "nmfb_dense_residual_kmajor": 2, "nmfb_tc_gemm": 1, "nmfb_split_transpose": 1, "nmfb_transpose": 1,
+    "nmfb_sum_parts": 1, "nmfb_dense_residual_kmajor": 2, "nmfb_csr_yt_chunked": 2, "nmfb_tc_gemm": 1, "nmfb_split_transpose": 1, "nmfb_transpose": 1,
 }
 
 

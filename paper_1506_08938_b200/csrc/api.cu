@@ -37,6 +37,9 @@ int dot_launch(const void *a, int a_dtype, const void *b, int b_dtype, int64_t l
 int add_into_launch(int dtype, void *dst, const void *src, int64_t len, int upper_r,
                     cudaStream_t st);
 int sum_parts_launch(const float *parts, int S, int64_t len, float *out, cudaStream_t st);
+int csr_yt_chunked_launch(int dtype, const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                          int64_t nheavy, const int32_t *colidx, const void *vals, const void *FT,
+                          int r, int yt_dtype, void *YT, void *part, cudaStream_t st);
 int dense_residual_kmajor_launch(const float *XT, int64_t m, int64_t n, const float *Gt,
                                  const float *Ft, int r, double *out, void *ws, cudaStream_t st);
 int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
@@ -214,6 +217,13 @@ int nmfb_dense_residual(int dtype, const void *XT, int64_t m, int64_t n, const v
                         const void *FT, int32_t r, double *out, void *workspace, void *stream) {
     return check(dense_residual_launch(dtype, XT, m, n, G, FT, r, out, workspace,
                                        (cudaStream_t)stream));
+}
+
+int nmfb_csr_yt_chunked(int dtype, const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                        int64_t nheavy, const int32_t *colidx, const void *vals, const void *FT,
+                        int32_t r, int yt_dtype, void *YT, void *part, void *stream) {
+    return check(csr_yt_chunked_launch(dtype, chunks, nchunks, heavy, nheavy, colidx, vals, FT, r,
+                                       yt_dtype, YT, part, (cudaStream_t)stream));
 }
 
 int nmfb_dense_residual_kmajor(const float *XT, int64_t m, int64_t n, const float *Gt,

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(128) csc_linear_kernel(const int64_t *__restri
             myrow = rowidx[base + lane];
             myv = vals[base + lane];
         }
+#pragma unroll 4
         for (int u = 0; u < cnt; ++u) {
             const int row = __shfl_sync(NMFB_FULL_MASK, myrow, u);
             const T v = __shfl_sync(NMFB_FULL_MASK, myv, u);
@@ -211,6 +212,114 @@ int csr_yt_launch(int dtype, int mode, const int64_t *rowptr, const int32_t *col
     return exact ? csr_yt_dispatch<float, float, true>(rowptr, colidx, vals, n, FT, r, sh, YT, st)
                  : csr_yt_dispatch<float, float, false>(rowptr, colidx, vals, n, FT, r, sh, YT,
                                                         st);
+}
+
+// Load-balanced Y^T pass (production): Zipf row popularity makes a few rows
+// hold 10^4+ nonzeros, so rows are cut into chunks of <= NMFB_CSR_CHUNK
+// entries (plan built once per matrix).  A warp sums one chunk (fp64 or fp32
+// accumulator); single-chunk rows are written directly, multi-chunk ("heavy")
+// rows go through partial slots that a second kernel folds in chunk order
+// (deterministic).  chunks: [nchunks][4] = (row, lo, hi, slot or -1);
+// heavy: [nheavy][3] = (row, first slot, count).
+template <typename T, typename TY, int C>
+__global__ void __launch_bounds__(128) csr_yt_chunk_kernel(const int64_t *__restrict__ chunks,
+                                                           int64_t nchunks,
+                                                           const int32_t *__restrict__ colidx,
+                                                           const T *__restrict__ vals,
+                                                           const T *__restrict__ FT, int r,
+                                                           TY *__restrict__ YT,
+                                                           TY *__restrict__ part) {
+    const int64_t ch = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (ch >= nchunks) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = chunks[ch * 4 + 0], p0 = chunks[ch * 4 + 1], p1 = chunks[ch * 4 + 2];
+    const int64_t slot = chunks[ch * 4 + 3];
+    TY acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = TY(0);
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int mycol = 0;
+        T myv = T(0);
+        if (lane < cnt) {
+            mycol = colidx[base + lane];
+            myv = vals[base + lane];
+        }
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+            const int col = __shfl_sync(NMFB_FULL_MASK, mycol, u);
+            const T v = __shfl_sync(NMFB_FULL_MASK, myv, u);
+            const T *f = FT + (int64_t)col * r;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int i = lane + 32 * c;
+                if (i < r) acc[c] = fma((TY)f[i], (TY)v, acc[c]);
+            }
+        }
+    }
+    TY *out = (slot < 0) ? (YT + row * r) : (part + slot * r);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int i = lane + 32 * c;
+        if (i < r) out[i] = acc[c];
+    }
+}
+
+template <typename TY>
+__global__ void csr_yt_fold_kernel(const int64_t *__restrict__ heavy, int64_t nheavy, int r,
+                                   const TY *__restrict__ part, TY *__restrict__ YT) {
+    const int64_t h = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (h >= nheavy) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = heavy[h * 3 + 0], first = heavy[h * 3 + 1], count = heavy[h * 3 + 2];
+    for (int i = lane; i < r; i += 32) {
+        TY s = TY(0);
+        for (int64_t k = 0; k < count; ++k) s += part[(first + k) * r + i];
+        YT[row * r + i] = s;
+    }
+}
+
+template <typename T, typename TY>
+static int csr_yt_chunked_dispatch(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                                   int64_t nheavy, const int32_t *colidx, const void *vals,
+                                   const void *FT, int r, void *YT, void *part, cudaStream_t st) {
+    dim3 grid((unsigned)((nchunks + 3) / 4));
+    const T *v = (const T *)vals;
+    const T *f = (const T *)FT;
+    TY *o = (TY *)YT, *pp = (TY *)part;
+#define NMFB_CSRC(Cc) \
+    csr_yt_chunk_kernel<T, TY, Cc><<<grid, 128, 0, st>>>(chunks, nchunks, colidx, v, f, r, o, pp)
+    if (r <= 32)
+        NMFB_CSRC(1);
+    else if (r <= 64)
+        NMFB_CSRC(2);
+    else if (r <= 128)
+        NMFB_CSRC(4);
+    else if (r <= 256)
+        NMFB_CSRC(8);
+    else
+        return NMFB_ERR_ARG;
+#undef NMFB_CSRC
+    if (nheavy > 0)
+        csr_yt_fold_kernel<TY><<<(unsigned)((nheavy + 3) / 4), 128, 0, st>>>(heavy, nheavy, r, pp,
+                                                                             o);
+    return launch_status();
+}
+
+int csr_yt_chunked_launch(int dtype, const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                          int64_t nheavy, const int32_t *colidx, const void *vals, const void *FT,
+                          int r, int yt_dtype, void *YT, void *part, cudaStream_t st) {
+    if (nchunks <= 0) return NMFB_OK;
+    if (dtype == NMFB_F64)
+        return yt_dtype == NMFB_F64
+                   ? csr_yt_chunked_dispatch<double, double>(chunks, nchunks, heavy, nheavy,
+                                                             colidx, vals, FT, r, YT, part, st)
+                   : NMFB_ERR_ARG;
+    return yt_dtype == NMFB_F64
+               ? csr_yt_chunked_dispatch<float, double>(chunks, nchunks, heavy, nheavy, colidx,
+                                                        vals, FT, r, YT, part, st)
+               : csr_yt_chunked_dispatch<float, float>(chunks, nchunks, heavy, nheavy, colidx,
+                                                       vals, FT, r, YT, part, st);
 }
 
 // Drop-in (nmfb_estep_sparse) accumulator: YT[row][i] += x[col][i] * v for the

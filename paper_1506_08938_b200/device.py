@@ -80,6 +80,34 @@ def block_plan(total, workers):
     return [(lo * b, min(hi * b, total)) for lo, hi in plan(nblocks, workers)]
 
 
+CSR_CHUNK = 256  # max nonzeros one warp sums in the load-balanced Y^T pass
+
+
+def csr_chunk_plan(rowptr, chunk=CSR_CHUNK):
+    """Row chunks for nmfb_csr_yt_chunked: (row, lo, hi, slot) per chunk, slot
+    -1 for single-chunk rows; heavy rows (row, first slot, count)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    n = len(rowptr) - 1
+    nnz_row = np.diff(rowptr)
+    nch = np.maximum(1, -(-nnz_row // chunk))
+    total = int(nch.sum())
+    row = np.repeat(np.arange(n, dtype=np.int64), nch)
+    first = np.cumsum(nch) - nch
+    within = np.arange(total, dtype=np.int64) - np.repeat(first, nch)
+    lo = rowptr[row] + within * chunk
+    hi = np.minimum(lo + chunk, rowptr[row + 1])
+    heavy_mask_rows = nch > 1
+    slot = np.full(total, -1, dtype=np.int64)
+    in_heavy = np.repeat(heavy_mask_rows, nch)
+    slot[in_heavy] = np.arange(int(in_heavy.sum()), dtype=np.int64)
+    chunks = np.stack([row, lo, hi, slot], axis=1).astype(np.int64)
+    hrows = np.flatnonzero(heavy_mask_rows).astype(np.int64)
+    hfirst = slot[first[hrows]] if len(hrows) else np.zeros(0, dtype=np.int64)
+    heavy = np.stack([hrows, hfirst, nch[hrows]], axis=1).astype(np.int64) if len(hrows) \
+        else np.zeros((0, 3), dtype=np.int64)
+    return np.ascontiguousarray(chunks), np.ascontiguousarray(heavy), int(in_heavy.sum())
+
+
 def shard_bounds(total, workers):
     shards = block_plan(total, workers)
     return [shards[0][0]] + [hi for _, hi in shards]
@@ -122,6 +150,10 @@ class DeviceData:
             self.rowptr = torch.from_numpy(rowptr).to(self.device)
             self.colidx = torch.from_numpy(colidx.astype(np.int32)).to(self.device)
             self.cvals = torch.from_numpy(cvals).to(self.device, dt)
+            chunks, heavy, nslots = csr_chunk_plan(rowptr)
+            self.chunks = torch.from_numpy(chunks).to(self.device)
+            self.heavy = torch.from_numpy(heavy).to(self.device)
+            self.nchunks, self.nheavy, self.nslots = len(chunks), len(heavy), nslots
             self.xsq = V.sum_squares()
             self.nnz = V.nnz
             self.host = V
@@ -336,8 +368,17 @@ class Alternation:
                        vp(self.ybuf), self._st())
         else:
             ycode = L.F64 if self.ybuf.dtype == torch.float64 else L.F32
-            L.call("nmfb_csr_yt", self.code, self.mode, vp(d.rowptr), vp(d.colidx), vp(d.cvals),
-                   n, vp(self.FT), r, ycode, bp, W, vp(self.ybuf), self._st())
+            if self.mode == L.MODE_FAST:
+                # load-balanced row chunks (Zipf-popular rows hold 10^4+ entries)
+                if getattr(self, "ypart", None) is None:
+                    self.ypart = torch.empty((max(d.nslots, 1) * r,), dtype=self.ybuf.dtype,
+                                             device=self.ybuf.device)
+                L.call("nmfb_csr_yt_chunked", self.code, vp(d.chunks), d.nchunks, vp(d.heavy),
+                       d.nheavy, vp(d.colidx), vp(d.cvals), vp(self.FT), r, ycode,
+                       vp(self.ybuf), vp(self.ypart), self._st())
+            else:
+                L.call("nmfb_csr_yt", self.code, self.mode, vp(d.rowptr), vp(d.colidx),
+                       vp(d.cvals), n, vp(self.FT), r, ycode, bp, W, vp(self.ybuf), self._st())
         del ba
 
     def mstep(self, k):

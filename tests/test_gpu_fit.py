@@ -211,3 +211,59 @@ def test_fit_regularized_fp32_teacher_forced_sparsity():
     for k, rel, eg, ef, zeq in res:
         assert rel < 1e-3, (k, rel)
         assert zeq.mean() > 0.97, (k, zeq.mean())
+
+
+def _product_sparse(csc):
+    from paper_1506_08938_b200 import SparseMatrix
+
+    return SparseMatrix(csc.rows, csc.cols, csc.indptr, csc.indices, csc.values, validate=False)
+
+
+def test_sparse_zipf_fp32_teacher_forced():
+    """Config-3 structure at small size (Zipf rows: popular rows exceed the
+    256-entry chunk, so the load-balanced Y^T pass splits and folds them)."""
+    from paper_1506_08938_b200 import NmfConfig
+    from paper_1506_08938_b200.nmf import FitSession
+
+    X = generators.sparse_zipf(3000, 2000, 0.01, 7)
+    assert np.diff(X.transpose().indptr).max() > 256
+    ocfg = orc.Config(rank=20, seed=7, rel_change_tol=0.0, max_outer=1)
+    gcfg = NmfConfig(rank=20, seed=7, rel_change_tol=0.0, max_outer=1, precision="fp32")
+    G, FT = orc.initial_factors(X, ocfg)
+    for k in range(6):
+        nG, nFT, obj, _, _, _ = orc.one_iteration(X, G, FT, ocfg)
+        if k in (0, 2, 5):
+            model, log = FitSession(_product_sparse(X), gcfg, init=(G, FT)).run()
+            assert abs(log.objective[0] - obj) / obj < 1e-4, (k, log.objective[0], obj)
+        G, FT = nG, nFT
+
+
+def test_sparse_zipf_fp64_bit_exact_with_reference_gram():
+    """fp64 check mode on Zipf sparse data, 10 iterations, with the oracle's
+    BLAS Gram fed in (the only op whose summation order OpenBLAS owns):
+    factors and inner-iteration counts bit-identical to the oracle.  (Free
+    running, the Gram's last-bit difference flips a few near-tie CD decisions
+    in the first component step on this data -- the SURVEY 0.6 sensitivity.)"""
+    import torch
+
+    from paper_1506_08938_b200 import NmfConfig
+    from paper_1506_08938_b200 import device as D
+    from paper_1506_08938_b200.nmf import initial_factors
+
+    X = generators.sparse_zipf(1500, 1000, 0.01, 8)
+    V = _product_sparse(X)
+    kw = dict(rank=12, seed=8, rel_change_tol=0.0, max_outer=10)
+    cfg = NmfConfig(precision="fp64", **kw)
+    G0, FT0 = initial_factors(V, cfg)
+    st = D.Alternation(D.DeviceData(V, "fp64"), cfg, G0, FT0, 10, precision="fp64")
+    objs = []
+    for k in range(10):
+        st.Qg.copy_(torch.from_numpy(orc.gram(st.G.cpu().numpy())))
+        st.qg_valid = True
+        st.iterate(k)
+        objs.append(st.assemble(st.pieces[k].cpu().numpy(), cfg, "sparse", X.sum_squares()))
+    oG, oFT, olog = orc.fit(X, orc.Config(**kw))
+    assert np.array_equal(st.stats[:, :, 0].sum(1).cpu().numpy(), olog.inner_iterations)
+    assert np.array_equal(st.G.cpu().numpy(), oG)
+    assert np.array_equal(st.FT.cpu().numpy(), oFT)
+    np.testing.assert_allclose(objs, olog.objective, rtol=1e-10)
