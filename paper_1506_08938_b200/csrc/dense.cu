@@ -401,50 +401,85 @@ __global__ void __launch_bounds__(256, 2) residual_f32_kernel(const float *__res
 #pragma unroll
         for (int v = 0; v < 8; ++v) acc[u][v] = 0.f;
     for (int kb = 0; kb < r; kb += R2K) {
-        for (int idx = tid; idx < R2K * R2T; idx += 256) {
-            const int kk = idx / R2T, t = idx % R2T;
+        // float4 row copies (4 per thread per operand); scalar tail guards
+        for (int idx = tid; idx < R2K * (R2T / 4); idx += 256) {
+            const int kk = idx >> 5, t4 = (idx & 31) * 4;
             const int gk = kb + kk;
-            const int64_t gj = j0 + t, gr = r0 + t;
-            Fs[kk][t] = (gj < m && gk < r) ? Ft[(int64_t)gk * m + gj] : 0.f;
-            Gs[kk][t] = (gr < n && gk < r) ? Gt[(int64_t)gk * n + gr] : 0.f;
+            const int64_t gj = j0 + t4, gr = r0 + t4;
+            float4 fv = make_float4(0.f, 0.f, 0.f, 0.f), gv = fv;
+            if (gk < r) {
+                const float *fp = Ft + (int64_t)gk * m + gj;
+                const float *gp = Gt + (int64_t)gk * n + gr;
+                if ((m % 4) == 0 && gj + 3 < m) {
+                    fv = *reinterpret_cast<const float4 *>(fp);
+                } else {
+                    fv.x = (gj < m) ? fp[0] : 0.f;
+                    fv.y = (gj + 1 < m) ? fp[1] : 0.f;
+                    fv.z = (gj + 2 < m) ? fp[2] : 0.f;
+                    fv.w = (gj + 3 < m) ? fp[3] : 0.f;
+                }
+                if ((n % 4) == 0 && gr + 3 < n) {
+                    gv = *reinterpret_cast<const float4 *>(gp);
+                } else {
+                    gv.x = (gr < n) ? gp[0] : 0.f;
+                    gv.y = (gr + 1 < n) ? gp[1] : 0.f;
+                    gv.z = (gr + 2 < n) ? gp[2] : 0.f;
+                    gv.w = (gr + 3 < n) ? gp[3] : 0.f;
+                }
+            }
+            *reinterpret_cast<float4 *>(&Fs[kk][t4]) = fv;
+            *reinterpret_cast<float4 *>(&Gs[kk][t4]) = gv;
         }
         __syncthreads();
         const int kmax = min(R2K, r - kb);
+#pragma unroll 4
         for (int kk = 0; kk < kmax; ++kk) {
             const float4 a0 = *reinterpret_cast<const float4 *>(&Fs[kk][ty * 8]);
             const float4 a1 = *reinterpret_cast<const float4 *>(&Fs[kk][ty * 8 + 4]);
-            const float4 b0 = *reinterpret_cast<const float4 *>(&Gs[kk][tx * 8]);
-            const float4 b1 = *reinterpret_cast<const float4 *>(&Gs[kk][tx * 8 + 4]);
+            // thread columns {4tx..4tx+3} u {64+4tx..}: 16 lanes read 256
+            // contiguous bytes per float4 load (no 32-byte-stride conflicts)
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Gs[kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Gs[kk][64 + tx * 4]);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const float2 b2[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                                  make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
+            // sm_100 packed FFMA2: two round-to-nearest FMAs per instruction
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < 8; ++u) {
+                const float2 au = make_float2(a[u], a[u]);
 #pragma unroll
-                for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
+                for (int v = 0; v < 4; ++v) {
+                    float2 c = make_float2(acc[u][2 * v], acc[u][2 * v + 1]);
+                    c = __ffma2_rn(au, b2[v], c);
+                    acc[u][2 * v] = c.x;
+                    acc[u][2 * v + 1] = c.y;
+                }
+            }
         }
         __syncthreads();
     }
     double s = 0.0;
-    const bool vec = (n % 4 == 0) && (r0 + tx * 8 + 7 < n);
+    auto colof = [&](int v) { return r0 + (v < 4 ? tx * 4 + v : 64 + tx * 4 + (v - 4)); };
+    const bool vec = (n % 4 == 0) && (colof(7) < n);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         const int64_t gj = j0 + ty * 8 + u;
         if (gj >= m) continue;
-        const float *xrow = XT + gj * n + r0 + tx * 8;
+        const float *xrow = XT + gj * n;
         float x[8];
         if (vec) {
-            const float4 x0 = *reinterpret_cast<const float4 *>(xrow);
-            const float4 x1 = *reinterpret_cast<const float4 *>(xrow + 4);
+            const float4 x0 = *reinterpret_cast<const float4 *>(xrow + colof(0));
+            const float4 x1 = *reinterpret_cast<const float4 *>(xrow + colof(4));
             x[0] = x0.x; x[1] = x0.y; x[2] = x0.z; x[3] = x0.w;
             x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
         } else {
 #pragma unroll
-            for (int v = 0; v < 8; ++v) x[v] = (r0 + tx * 8 + v < n) ? xrow[v] : 0.f;
+            for (int v = 0; v < 8; ++v) x[v] = (colof(v) < n) ? xrow[colof(v)] : 0.f;
         }
         float su = 0.f;
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-            if (r0 + tx * 8 + v < n) {
+            if (colof(v) < n) {
                 const float d = x[v] - acc[u][v];
                 su = fmaf(d, d, su);
             }

@@ -57,3 +57,26 @@ def test_tc_gemm_stage_depths_agree(stages):
     C0, _ = _tc(A, B, 2, stages=4)
     C1, _ = _tc(A, B, 2, stages=stages)
     assert np.array_equal(C0, C1)  # same tiles, same order -> bit-identical
+
+
+@pytest.mark.parametrize("m,n,r", [(130, 77, 5), (256, 384, 50), (1000, 500, 64), (300, 1030, 37)])
+def test_dense_residual_kmajor_matches_fp64(m, n, r):
+    """0.5 ||X - G F||^2 from the k-major operands, fp32 FFMA + fp64 sums."""
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    rng = np.random.default_rng(m + n + r)
+    G = rng.uniform(size=(n, r)).astype(np.float32)
+    F = rng.uniform(size=(r, m)).astype(np.float32)
+    X = (G.astype(np.float64) @ F + rng.normal(0, 0.1, size=(n, m))).astype(np.float32)
+    XT = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)
+    Gt = torch.from_numpy(np.ascontiguousarray(G.T)).to(dev)
+    Ft = torch.from_numpy(np.ascontiguousarray(F)).to(dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    ws = torch.empty((L.lib().nmfb_residual_workspace_bytes(m, n) // 8 + 1,),
+                     dtype=torch.float64, device=dev)
+    L.call("nmfb_dense_residual_kmajor", D.vp(XT), m, n, D.vp(Gt), D.vp(Ft), r, D.vp(out),
+           D.vp(ws), D.stream_handle())
+    want = 0.5 * np.sum((X.astype(np.float64) - G.astype(np.float64) @ F.astype(np.float64)) ** 2)
+    assert abs(float(out.item()) - want) / want < 1e-5
