@@ -157,12 +157,17 @@ int nmfb_gemm_tall(const float *A, int a_kmajor, int64_t M, int64_t K, int64_t l
 
 /* Tensor-core (tcgen05, kind::tf32, 3xTF32 split) split-K GEMM:
  * C[s] (M x N row-major) = A(M x K, K contiguous) * Bt(N x K, K contiguous)^T
- * over the s-th K chunk.  Bt_lo = Bt - tf32(Bt) (nmfb_split_transpose makes
- * both from a K x N row-major B).  K % 4 == 0, N <= 160, 16-byte aligned
- * pointers.  stages: smem pipeline depth (0 = auto).  The number of K
- * chunks actually used is nmfb_tc_splits(K, splits). */
+ * over the s-th K part, so sum_s C[s] = A Bt^T.  Bt_lo = Bt - tf32(Bt)
+ * (nmfb_split_transpose makes both from a K x N row-major B).  K % 4 == 0,
+ * N <= 160, 16-byte aligned pointers.  splits > 0: fixed K chunks;
+ * splits <= 0: balanced schedule (every SM gets an equal run of 128 x 32
+ * k-blocks; a tile's parts are the runs that cover it, unused parts zeroed).
+ * C must hold nmfb_tc_parts(M, K, N, splits) * M * N floats.  stages: smem
+ * pipeline depth (0 = auto).  Deterministic for a given device. */
 int nmfb_tc_gemm(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
                  int32_t N, float *C, int32_t splits, int32_t stages, void *stream);
+int nmfb_tc_parts(int64_t M, int64_t K, int32_t N, int32_t splits);
+/* fixed-chunk count for splits > 0 (= nmfb_tc_parts for that case) */
 int nmfb_tc_splits(int64_t K, int32_t splits);
 /* B (K x r row-major) -> Bt_hi = B^T (r x K), Bt_lo = B^T - tf32(B^T). */
 int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, float *Bt_lo,

@@ -74,6 +74,7 @@ SIGNATURES = {
     "nmfb_sum_parts": (_int, [_vp, _i32, _i64, _vp, _vp]),
     "nmfb_tc_gemm": (_int, [_vp, _i64, _i64, _vp, _vp, _i32, _vp, _i32, _i32, _vp]),
     "nmfb_tc_splits": (_int, [_i64, _i32]),
+    "nmfb_tc_parts": (_int, [_i64, _i64, _i32, _i32]),
     "nmfb_split_transpose": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "nmfb_transpose": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "nmfb_dot": (_int, [_vp, _int, _vp, _int, _i64, _vp, _vp, _vp]),

@@ -45,6 +45,7 @@ int dense_residual_kmajor_launch(const float *XT, int64_t m, int64_t n, const fl
 int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
                    int N, float *C, int splits, int stages, cudaStream_t st);
 int tc_effective_splits(int64_t K, int splits);
+int tc_parts(int64_t M, int64_t K, int N, int splits);
 int split_transpose_launch(const float *B, int64_t K, int r, float *hi, float *lo,
                            cudaStream_t st);
 int transpose_launch(const float *in, int64_t rows, int64_t cols, float *out, cudaStream_t st);
@@ -246,6 +247,9 @@ int nmfb_tc_gemm(const float *A, int64_t M, int64_t K, const float *Bt_hi, const
 }
 
 int nmfb_tc_splits(int64_t K, int32_t splits) { return tc_effective_splits(K, splits); }
+int nmfb_tc_parts(int64_t M, int64_t K, int32_t N, int32_t splits) {
+    return tc_parts(M, K, N, splits);
+}
 
 int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, float *Bt_lo,
                          void *stream) {

@@ -86,24 +86,39 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const T *__restrict__
     }
 }
 
-// out[a][b] = out[b][a] = sum_c part[c][min(a,b)][max(a,b)] in chunk order.
-__global__ void gram_reduce_kernel(const double *__restrict__ part, int nchunk, int r,
-                                   double *__restrict__ out) {
-    int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= r * r) return;
-    int a = idx / r, b = idx % r;
-    int lo = min(a, b), hi = max(a, b);
+// out[a][b] = out[b][a] = sum_c part[c][a][b] (a <= b).  One CTA per 32
+// consecutive entries: warp w sums the chunks c = w (mod 8) in increasing c
+// (coalesced 256-byte rows), then the 8 warp sums are added in warp order --
+// a fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(256) gram_reduce_kernel(const double *__restrict__ part,
+                                                          int nchunk, int r,
+                                                          double *__restrict__ out) {
+    __shared__ double sh[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int idx = blockIdx.x * 32 + lane;
+    const int a = idx / r, b = idx % r;
+    const bool upper = idx < r * r && a <= b;
     double s = 0.0;
-    for (int c = 0; c < nchunk; ++c) s += part[(int64_t)c * r * r + lo * r + hi];
-    out[idx] = s;
+    if (upper)
+        for (int c = warp; c < nchunk; c += 8) s += part[(int64_t)c * r * r + idx];
+    sh[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && upper) {
+        double t = sh[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) t += sh[w][lane];
+        out[a * r + b] = t;
+        out[b * r + a] = t;
+    }
 }
 
 static int64_t gram_chunk(int64_t rows) {
-    // ~2 waves of 148 SMs worth of chunks, each a multiple of the slab height
+    // ~2 chunks per SM (148 SMs), each a whole number of GROWS-row slabs; the
+    // reduce is parallel over entries, so many chunks cost little
     int64_t target = 296;
     int64_t chunk = (rows + target - 1) / target;
     chunk = ((chunk + GROWS - 1) / GROWS) * GROWS;
-    if (chunk < 256) chunk = 256;
+    if (chunk < GROWS) chunk = GROWS;
     return chunk;
 }
 
@@ -130,7 +145,7 @@ int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, doub
         gram_partial_kernel<float><<<grid, 256, 0, st>>>((const float *)A, rows, r, lda, chunk,
                                                          part);
     }
-    gram_reduce_kernel<<<(r * r + 255) / 256, 256, 0, st>>>(part, (int)nchunk, r, out);
+    gram_reduce_kernel<<<(r * r + 31) / 32, 256, 0, st>>>(part, (int)nchunk, r, out);
     return launch_status();
 }
 

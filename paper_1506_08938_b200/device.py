@@ -237,8 +237,10 @@ class Alternation:
         if data.kind == "dense" and self.mode == L.MODE_FAST:
             if self.use_tc:
                 data.ensure_x_rowmajor()
-                self.splits_e = splits or L.lib().nmfb_tc_splits(n, self._tc_splits(m, sms))
-                self.splits_m = splits or L.lib().nmfb_tc_splits(m, self._tc_splits(n, sms))
+                # balanced persistent schedule (splits <= 0) unless a split count is forced
+                self.tc_req = int(splits or 0)
+                self.splits_e = L.lib().nmfb_tc_parts(m, n, r, self.tc_req)
+                self.splits_m = L.lib().nmfb_tc_parts(n, m, r, self.tc_req)
                 # [iteration parity][hi, lo] k-major tf32 splits of G^T and F; two
                 # parities so the residual of iteration k (side stream) can still
                 # read its operands while iteration k+1 runs
@@ -270,12 +272,6 @@ class Alternation:
         self.qg_valid = False
         self.index_base_e = 0  # global column of FT row 0 (multi-GPU column shards)
         self.gt_valid = False  # Gt holds tf32-split G^T of the current G
-
-    @staticmethod
-    def _tc_splits(M, sms):
-        # one 128-row tile per CTA, 1 CTA/SM: ~8 waves keeps the tail short
-        tiles = -(-M // 128)
-        return int(max(1, min(16, round(8 * sms / tiles))))
 
     @staticmethod
     def _splits(M, K, sms):
@@ -331,7 +327,7 @@ class Alternation:
                            self._st())
                 self.gt_valid = False
                 L.call("nmfb_tc_gemm", vp(d.XT), m, n, vp(Gt[0]), vp(Gt[1]), r,
-                       vp(self.hbuf), self.splits_e, 0, self._st())
+                       vp(self.hbuf), self.tc_req, 0, self._st())
                 self.nnls(0, self.hbuf, L.F32, self.splits_e, r, m * r, cfg.mu1, self.FT, m, st)
             elif self.mode == L.MODE_FAST:
                 L.call("nmfb_gemm_tall", vp(d.XT), 1, m, n, n, vp(self.G), r, r, vp(self.hbuf),
@@ -359,7 +355,7 @@ class Alternation:
                 L.call("nmfb_split_transpose", vp(self.FT), m, r, vp(Ft[0]), vp(Ft[1]),
                        self._st())
                 L.call("nmfb_tc_gemm", vp(d.X), n, m, vp(Ft[0]), vp(Ft[1]), r,
-                       vp(self.ybuf), self.splits_m, 0, self._st())
+                       vp(self.ybuf), self.tc_req, 0, self._st())
             elif self.mode == L.MODE_FAST:
                 L.call("nmfb_gemm_tall", vp(d.XT), 0, n, m, n, vp(self.FT), r, r,
                        vp(self.ybuf), self.splits_m, self._st())

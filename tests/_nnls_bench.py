@@ -22,7 +22,7 @@ d = st.d
 FT0 = st.FT.clone()
 if d.kind == "dense":
     L.call("nmfb_split_transpose", D.vp(st.G), st.n, st.r, D.vp(st.Gt[0]), D.vp(st.Gt[1]), D.stream_handle())
-    L.call("nmfb_tc_gemm", D.vp(d.XT), st.m, st.n, D.vp(st.Gt[0]), D.vp(st.Gt[1]), st.r, D.vp(st.hbuf), st.splits_e, 0, D.stream_handle())
+    L.call("nmfb_tc_gemm", D.vp(d.XT), st.m, st.n, D.vp(st.Gt[0]), D.vp(st.Gt[1]), st.r, D.vp(st.hbuf), st.tc_req, 0, D.stream_handle())
     args = (st.hbuf, L.F32, st.splits_e, st.r, st.m * st.r, 0.0)
 else:
     L.call("nmfb_csc_linear", st.code, st.mode, D.vp(d.indptr), D.vp(d.rowidx), D.vp(d.vals), 0, st.m, D.vp(st.G), st.r, 0.0, D.vp(st.hbuf), D.stream_handle())

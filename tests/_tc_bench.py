@@ -16,17 +16,18 @@ for (M, K, N) in [(20000, 10000, 50), (10000, 20000, 50), (20000, 20000, 64)]:
     B = torch.rand((K, N), device=dev)
     Bt = torch.empty((N, K), device=dev); Btl = torch.empty((N, K), device=dev)
     L.call("nmfb_split_transpose", D.vp(B), K, N, D.vp(Bt), D.vp(Btl), D.stream_handle())
-    for S in [1, 2, 4, 8, 15]:
-        for stages in [2, 4]:
-            Ss = L.lib().nmfb_tc_splits(K, S)
+    for S in [0, 8]:
+        for stages in [2, 4, 6]:
+            Ss = L.lib().nmfb_tc_parts(M, K, N, S)
             C = torch.empty((Ss, M, N), device=dev)
             ms = timeit(lambda: L.call("nmfb_tc_gemm", D.vp(A), M, K, D.vp(Bt), D.vp(Btl), N, D.vp(C), S, stages, D.stream_handle()))
-            print(f"tc   M={M} K={K} N={N} S={S} stages={stages}: {ms:.3f} ms  {M*K*4/ms/1e6:.0f} GB/s", flush=True)
+            print(f"tc   M={M} K={K} N={N} S={S}/{Ss} stages={stages}: {ms:.3f} ms  {M*K*4/ms/1e6:.0f} GB/s", flush=True)
     Cs = torch.empty((4, M, N), device=dev)
     ms = timeit(lambda: L.call("nmfb_gemm_tall", D.vp(A), 1, M, K, K, D.vp(B), N, N, D.vp(Cs), 4, D.stream_handle()))
     print(f"simt M={M} K={K} N={N} S=4: {ms:.3f} ms  {M*K*4/ms/1e6:.0f} GB/s", flush=True)
     ref = (A.double() @ B.double())
-    C = torch.empty((1, M, N), device=dev)
-    L.call("nmfb_tc_gemm", D.vp(A), M, K, D.vp(Bt), D.vp(Btl), N, D.vp(C), 1, 0, D.stream_handle())
+    Ss = L.lib().nmfb_tc_parts(M, K, N, 0)
+    C = torch.empty((Ss, M, N), device=dev)
+    L.call("nmfb_tc_gemm", D.vp(A), M, K, D.vp(Bt), D.vp(Btl), N, D.vp(C), 0, 0, D.stream_handle())
     torch.cuda.synchronize()
-    print("  max rel err tc", float(((C[0].double() - ref).abs() / ref.abs()).max()))
+    print("  max rel err tc", float(((C.double().sum(0) - ref).abs() / ref.abs()).max()))

@@ -2,8 +2,10 @@
 same op (the dense passes G^T X and X F^T).  Tolerance: 3xTF32 carries ~21
 mantissa bits per product, accumulation in fp32 -> 2e-5 relative to the
 magnitude scale of the output (|A||B|).  The tensor core's fp32 accumulate
-truncates, so the kernel folds every 2 k-blocks into a round-to-nearest
-running sum; the error must not grow with K."""
+truncates, so the kernel folds every few k-blocks into a round-to-nearest
+running sum; the error must not grow with K.  splits <= 0 selects the balanced
+(stream-K style) schedule: its unused partial slots must come back zeroed
+(the output buffer starts as NaN)."""
 
 import numpy as np
 import pytest
@@ -25,7 +27,7 @@ def _tc(A, B, splits=1, stages=0):
     bt_hi = torch.empty((N, K), dtype=torch.float32, device=dev)
     bt_lo = torch.empty((N, K), dtype=torch.float32, device=dev)
     L.call("nmfb_split_transpose", D.vp(b), K, N, D.vp(bt_hi), D.vp(bt_lo), D.stream_handle())
-    S = L.lib().nmfb_tc_splits(K, splits)
+    S = L.lib().nmfb_tc_parts(M, K, N, splits)
     C = torch.full((S, M, N), float("nan"), dtype=torch.float32, device=dev)
     L.call("nmfb_tc_gemm", D.vp(a), M, K, D.vp(bt_hi), D.vp(bt_lo), N, D.vp(C), splits, stages,
            D.stream_handle())
@@ -36,6 +38,8 @@ def _tc(A, B, splits=1, stages=0):
 @pytest.mark.parametrize("M,K,N,splits", [
     (128, 32, 16, 1), (256, 64, 50, 1), (300, 1000, 50, 3), (1000, 4096, 64, 4),
     (20000, 1024, 50, 2), (77, 96, 10, 1), (513, 2000, 100, 5), (256, 512, 160, 2), (300, 10000, 50, 1),
+    (128, 32, 16, 0), (300, 1000, 50, 0), (20000, 1024, 50, 0), (10000, 4000, 50, 0),
+    (513, 2000, 100, 0), (256, 512, 160, 0), (77, 96, 10, 0), (40000, 64, 33, 0), (1000, 20000, 64, 0),
 ])
 def test_tc_gemm_matches_fp64(M, K, N, splits):
     rng = np.random.default_rng(M + K + N)
@@ -57,6 +61,17 @@ def test_tc_gemm_stage_depths_agree(stages):
     C0, _ = _tc(A, B, 2, stages=4)
     C1, _ = _tc(A, B, 2, stages=stages)
     assert np.array_equal(C0, C1)  # same tiles, same order -> bit-identical
+
+
+def test_tc_gemm_balanced_deterministic():
+    rng = np.random.default_rng(9)
+    A = rng.uniform(size=(3000, 5000))
+    B = rng.uniform(size=(5000, 50))
+    C0, S0 = _tc(A, B, 0)
+    C1, S1 = _tc(A, B, 0)
+    assert S0 == S1 and np.array_equal(C0, C1)
+    C2, _ = _tc(A, B, 4)
+    assert np.abs(C2 - C0).max() / np.abs(C0).max() < 1e-6
 
 
 @pytest.mark.parametrize("m,n,r", [(130, 77, 5), (256, 384, 50), (1000, 500, 64), (300, 1030, 37)])
