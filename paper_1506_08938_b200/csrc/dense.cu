@@ -395,6 +395,12 @@ __global__ void __launch_bounds__(256, 2) residual_f32_kernel(const float *__res
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int64_t j0 = (int64_t)blockIdx.y * R2T;  // m
     const int64_t r0 = (int64_t)blockIdx.x * R2T;  // n
+    // warm L2 with this CTA's X tile (128 rows x 512 B) so the epilogue's
+    // reads do not pay HBM latency after the k-loop
+    for (int l = tid; l < R2T * 4; l += 256) {
+        const int64_t gj = j0 + (l >> 2), gr = r0 + (l & 3) * 32;
+        if (gj < m && gr < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(XT + gj * n + gr));
+    }
     float acc[8][8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)

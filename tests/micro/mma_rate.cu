@@ -18,6 +18,12 @@ __device__ __forceinline__ void umma_f16(uint32_t d, uint64_t a, uint64_t b, uin
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc));
 }
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc));
+}
 // mode 0: one accumulator; 1: 4 rotating accumulators; 2: commit+wait every 4
 // kind 0: tf32, 1: bf16; M = 128
 __global__ void mma_rate(long long *out, int N, int iters, int mode, int kind) {
@@ -38,8 +44,9 @@ __global__ void mma_rate(long long *out, int N, int iters, int mode, int kind) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = slot;
     if (threadIdx.x == 0) {
-        const uint32_t fmt = kind == 0 ? 2u : 1u;
-        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) |
+        const uint32_t fmt = kind == 0 ? 2u : (kind == 1 ? 1u : 0u);
+        const uint32_t cfmt = kind == 2 ? 2u : 1u;
+        const uint32_t idesc = (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
         const uint64_t a = umma_desc_sw128(sm), b = umma_desc_sw128(sm + 16384);
         uint32_t ph = 0;
@@ -49,8 +56,10 @@ __global__ void mma_rate(long long *out, int N, int iters, int mode, int kind) {
             const uint64_t dk = (uint64_t)((it & 3) * 2);
             if (kind == 0)
                 umma_tf32(d, a + dk, b + dk, idesc, 1u);
-            else
+            else if (kind == 1)
                 umma_f16(d, a + dk, b + dk, idesc);
+            else
+                umma_i8(d, a + dk, b + dk, idesc);
             if (mode == 2 && (it & 3) == 3) {
                 umma_commit(&bar);
                 mbar_wait(&bar, ph);
@@ -76,17 +85,17 @@ int main() {
     cudaMalloc(&d, 16);
     cudaFuncSetAttribute(nmfb::mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     const int iters = 4096;
-    for (int kind = 0; kind < 2; ++kind)
-        for (int mode = 0; mode < 3; ++mode)
+    for (int kind = 0; kind < 3; ++kind)
+        for (int mode = 0; mode < 2; ++mode)
             for (int N : {16, 32, 64, 128, 256}) {
                 nmfb::mma_rate<<<1, 128, 100 * 1024>>>(d, N, iters, mode, kind);
                 nmfb::mma_rate<<<1, 128, 100 * 1024>>>(d, N, iters, mode, kind);
                 cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
                 double ns = (double)h[1] / iters;
-                double flops = 2.0 * 128 * N * (kind == 0 ? 8 : 16);
+                double flops = 2.0 * 128 * N * (kind == 0 ? 8 : (kind == 1 ? 16 : 32));
                 printf("%s mode=%d N=%3d: issue %.1f ns/mma, complete %.1f ns/mma, %.1f TFLOP/s/SM "
                        "(x148 = %.0f TF/s)\n",
-                       kind == 0 ? "tf32" : "bf16", mode, N, (double)h[0] / iters, ns,
+                       kind == 0 ? "tf32" : (kind == 1 ? "bf16" : "u8  "), mode, N, (double)h[0] / iters, ns,
                        flops / ns / 1e3, flops / ns / 1e3 * 148);
             }
     cudaError_t e = cudaDeviceSynchronize();
