@@ -228,6 +228,21 @@ int nmfb_dense_residual_kmajor(const float *XT, int64_t m, int64_t n, const floa
                                const float *Ft, int32_t r, double *out, void *workspace,
                                void *stream);
 
+/* Exact-product residual on the int8 tensor cores (G, F >= 0).  Per iteration
+ * the factors are cut into three 8-bit slices with a power-of-two scale per
+ * row: nmfb_slice_u8(A rows x r, lda) writes nmfb_slice_bytes(rows, r) bytes
+ * (3 x rows x KB u8 slices, KB = 64 if r <= 64 else 128, then rows float
+ * scales); r <= 128.
+ * nmfb_residual_i8 adds 0.5 ||X - G F||^2 to *out (device double) with
+ * X (n x m) row-major, m % 4 == 0, Gsl = slices of G (n x r), Fsl = slices of
+ * F^T (m x r).  G F is exact up to the 2^-24 slicing; X - G F is formed and
+ * squared in fp32 (round-to-nearest), summed in fp64, deterministically. */
+size_t nmfb_slice_bytes(int64_t rows, int32_t r);
+int nmfb_slice_u8(const float *A, int64_t rows, int32_t r, int64_t lda, void *out, void *stream);
+size_t nmfb_residual_i8_workspace_bytes(void);
+int nmfb_residual_i8(const float *X, int64_t n, int64_t m, const void *Gsl, const void *Fsl,
+                     int32_t r, double *out, void *workspace, void *stream);
+
 /* out[i] = sum_{s < S} parts[s * len + i], fixed order (split-K partials of
  * X F^T summed before the multi-GPU reduce-scatter).  float32. */
 int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void *stream);

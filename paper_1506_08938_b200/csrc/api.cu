@@ -45,6 +45,11 @@ int dense_residual_kmajor_launch(const float *XT, int64_t m, int64_t n, const fl
 int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
                    int N, float *C, int splits, int stages, cudaStream_t st);
 int tc_effective_splits(int64_t K, int splits);
+size_t slice_bytes(int64_t rows, int r);
+int slice_u8_launch(const float *A, int64_t rows, int r, int64_t lda, void *out, cudaStream_t st);
+size_t residual_i8_workspace_bytes();
+int residual_i8_launch(const float *X, int64_t n, int64_t m, const void *Gsl, const void *Fsl,
+                       int r, double *out, void *ws, cudaStream_t st);
 int tc_parts(int64_t M, int64_t K, int N, int splits);
 int split_transpose_launch(const float *B, int64_t K, int r, float *hi, float *lo,
                            cudaStream_t st);
@@ -232,6 +237,16 @@ int nmfb_dense_residual_kmajor(const float *XT, int64_t m, int64_t n, const floa
                                void *stream) {
     return check(dense_residual_kmajor_launch(XT, m, n, Gt, Ft, r, out, workspace,
                                               (cudaStream_t)stream));
+}
+
+size_t nmfb_slice_bytes(int64_t rows, int32_t r) { return slice_bytes(rows, r); }
+int nmfb_slice_u8(const float *A, int64_t rows, int32_t r, int64_t lda, void *out, void *stream) {
+    return check(slice_u8_launch(A, rows, r, lda, out, (cudaStream_t)stream));
+}
+size_t nmfb_residual_i8_workspace_bytes(void) { return residual_i8_workspace_bytes(); }
+int nmfb_residual_i8(const float *X, int64_t n, int64_t m, const void *Gsl, const void *Fsl,
+                     int32_t r, double *out, void *workspace, void *stream) {
+    return check(residual_i8_launch(X, n, m, Gsl, Fsl, r, out, workspace, (cudaStream_t)stream));
 }
 
 size_t nmfb_dot_workspace_bytes(int64_t len) { return dot_workspace_bytes(len); }

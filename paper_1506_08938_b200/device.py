@@ -43,6 +43,13 @@ def tc_enabled():
     return os.environ.get("NMFB_DISABLE_TC", "0") != "1"
 
 
+def d_i8_enabled():
+    """Exact int8 tensor-core residual unless NMFB_DISABLE_I8=1 (A/B comparisons)."""
+    import os
+
+    return os.environ.get("NMFB_DISABLE_I8", "0") != "1"
+
+
 def require_cuda():
     L.lib()
     if not torch.cuda.is_available():
@@ -246,6 +253,16 @@ class Alternation:
                 # read its operands while iteration k+1 runs
                 self.Gt = torch.empty((2, 2, r, n), dtype=torch.float32, device=dev)
                 self.Ft = torch.empty((2, 2, r, m), dtype=torch.float32, device=dev)
+                # exact int8 tensor-core residual: per-parity 8-bit slices of G, F^T
+                self.use_i8 = (r <= 128 and m % 4 == 0 and d_i8_enabled())
+                if self.use_i8:
+                    lib = L.lib()
+                    self.Gsl = torch.empty((2, lib.nmfb_slice_bytes(n, r)), dtype=torch.uint8,
+                                           device=dev)
+                    self.Fsl = torch.empty((2, lib.nmfb_slice_bytes(m, r)), dtype=torch.uint8,
+                                           device=dev)
+                    self.rq_ws = torch.empty((lib.nmfb_residual_i8_workspace_bytes() // 8 + 1,),
+                                             dtype=f64, device=dev)
                 lo, hi = torch.cuda.Stream.priority_range()
                 self.main = torch.cuda.Stream(device=dev, priority=hi)
                 self.side = torch.cuda.Stream(device=dev, priority=lo)
@@ -402,14 +419,27 @@ class Alternation:
             L.call("nmfb_split_transpose", vp(self.G), self.n, self.r, vp(Gt[0]), vp(Gt[1]),
                    self._st())
             self.gt_valid = True
-            # the FFMA-bound residual runs on a side stream, overlapping the next
-            # iteration's HBM/smem-bound tensor-core pass and latency-bound NNLS
+            if self.use_i8:
+                # 8-bit slices of this iteration's G and F (snapshots: the side-stream
+                # residual reads them while the next iteration overwrites G, FT)
+                self._wait_residual(q)
+                L.call("nmfb_slice_u8", vp(self.G), self.n, self.r, self.r, vp(self.Gsl[q]),
+                       self._st())
+                L.call("nmfb_slice_u8", vp(self.FT), self.m, self.r, self.r, vp(self.Fsl[q]),
+                       self._st())
+            # the residual runs on a side stream, overlapping the next iteration
             ready = torch.cuda.Event()
             ready.record()
             self.side.wait_event(ready)
             with torch.cuda.stream(self.side):
-                L.call("nmfb_dense_residual_kmajor", vp(d.XT), self.m, self.n, vp(Gt[0]),
-                       vp(Ft[0]), self.r, vp(p[0:1]), vp(self.res_ws), stream_handle(self.side))
+                if self.use_i8:
+                    L.call("nmfb_residual_i8", vp(d.X), self.n, self.m, vp(self.Gsl[q]),
+                           vp(self.Fsl[q]), self.r, vp(p[0:1]), vp(self.rq_ws),
+                           stream_handle(self.side))
+                else:
+                    L.call("nmfb_dense_residual_kmajor", vp(d.XT), self.m, self.n, vp(Gt[0]),
+                           vp(Ft[0]), self.r, vp(p[0:1]), vp(self.res_ws),
+                           stream_handle(self.side))
                 ev = torch.cuda.Event()
                 ev.record(self.side)
             self.res_ev[q] = ev

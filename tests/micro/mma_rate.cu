@@ -26,7 +26,7 @@ __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint
 }
 // mode 0: one accumulator; 1: 4 rotating accumulators; 2: commit+wait every 4
 // kind 0: tf32, 1: bf16; M = 128
-__global__ void mma_rate(long long *out, int N, int iters, int mode, int kind) {
+__global__ void mma_rate(long long *out, int N, int iters, int mode, int kind, int sw64) {
     extern __shared__ __align__(1024) uint8_t raw[];
     uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t bar;
@@ -48,7 +48,11 @@ __global__ void mma_rate(long long *out, int N, int iters, int mode, int kind) {
         const uint32_t cfmt = kind == 2 ? 2u : 1u;
         const uint32_t idesc = (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
-        const uint64_t a = umma_desc_sw128(sm), b = umma_desc_sw128(sm + 16384);
+        uint64_t a = umma_desc_sw128(sm), b = umma_desc_sw128(sm + 16384);
+        if (sw64) {  // SWIZZLE_64B K-major: layout 4, SBO = 8 rows x 64 B
+            a = (a & ~(((uint64_t)0x3FFF << 32) | ((uint64_t)7 << 61))) | ((uint64_t)(512 >> 4) << 32) | ((uint64_t)4 << 61);
+            b = (b & ~(((uint64_t)0x3FFF << 32) | ((uint64_t)7 << 61))) | ((uint64_t)(512 >> 4) << 32) | ((uint64_t)4 << 61);
+        }
         uint32_t ph = 0;
         long long t0 = gt();
         for (int it = 0; it < iters; ++it) {
@@ -87,15 +91,16 @@ int main() {
     const int iters = 4096;
     for (int kind = 0; kind < 3; ++kind)
         for (int mode = 0; mode < 2; ++mode)
-            for (int N : {16, 32, 64, 128, 256}) {
-                nmfb::mma_rate<<<1, 128, 100 * 1024>>>(d, N, iters, mode, kind);
-                nmfb::mma_rate<<<1, 128, 100 * 1024>>>(d, N, iters, mode, kind);
+            for (int N : {16, 32, 64, 80, 128, 256})
+              for (int sw64 = 0; sw64 < 2; ++sw64) {
+                nmfb::mma_rate<<<1, 128, 100 * 1024>>>(d, N, iters, mode, kind, sw64);
+                nmfb::mma_rate<<<1, 128, 100 * 1024>>>(d, N, iters, mode, kind, sw64);
                 cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
                 double ns = (double)h[1] / iters;
                 double flops = 2.0 * 128 * N * (kind == 0 ? 8 : (kind == 1 ? 16 : 32));
-                printf("%s mode=%d N=%3d: issue %.1f ns/mma, complete %.1f ns/mma, %.1f TFLOP/s/SM "
+                printf("%s sw%d mode=%d N=%3d: issue %.1f ns/mma, complete %.1f ns/mma, %.1f TFLOP/s/SM "
                        "(x148 = %.0f TF/s)\n",
-                       kind == 0 ? "tf32" : (kind == 1 ? "bf16" : "u8  "), mode, N, (double)h[0] / iters, ns,
+                       kind == 0 ? "tf32" : (kind == 1 ? "bf16" : "u8  "), sw64 ? 64 : 128, mode, N, (double)h[0] / iters, ns,
                        flops / ns / 1e3, flops / ns / 1e3 * 148);
             }
     cudaError_t e = cudaDeviceSynchronize();

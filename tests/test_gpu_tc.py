@@ -95,3 +95,67 @@ def test_dense_residual_kmajor_matches_fp64(m, n, r):
            D.vp(ws), D.stream_handle())
     want = 0.5 * np.sum((X.astype(np.float64) - G.astype(np.float64) @ F.astype(np.float64)) ** 2)
     assert abs(float(out.item()) - want) / want < 1e-5
+
+
+def _slices(A):
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    rows, r = A.shape
+    a = torch.from_numpy(np.ascontiguousarray(A, dtype=np.float32)).to(dev)
+    out = torch.zeros((L.lib().nmfb_slice_bytes(rows, r),), dtype=torch.uint8, device=dev)
+    L.call("nmfb_slice_u8", D.vp(a), rows, r, r, D.vp(out), D.stream_handle())
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("rows,r", [(1, 1), (100, 50), (1000, 64), (333, 128), (77, 7)])
+def test_slice_u8_reconstructs(rows, r):
+    """Three 8-bit slices + a power-of-two row scale represent each row to
+    2^-24 of its max (the last slice rounded to nearest)."""
+    rng = np.random.default_rng(rows + r)
+    A = rng.exponential(size=(rows, r)).astype(np.float32)
+    A[rng.uniform(size=A.shape) < 0.3] = 0.0  # NNLS outputs are sparse
+    if rows > 2:
+        A[1] = 0.0  # an all-zero row
+        A[2] *= 1e-30  # tiny magnitudes
+    out = _slices(A).cpu().numpy()
+    kb = 64 if r <= 64 else 128
+    S = out[: 3 * rows * kb].reshape(3, rows, kb).astype(np.float64)
+    scale = out[3 * rows * kb: 3 * rows * kb + 4 * rows].view(np.float32).astype(np.float64)
+    assert (S[:, :, r:] == 0).all()
+    rec = (S[0] / 2.0**8 + S[1] / 2.0**16 + S[2] / 2.0**24)[:, :r] * scale[:, None]
+    mx = A.max(axis=1, keepdims=True).astype(np.float64)
+    err = np.abs(rec - A) / np.where(mx > 0, mx, 1.0)
+    assert err.max() <= 2.0**-24, err.max()
+    assert np.all(rec[A == 0] == 0)
+
+
+@pytest.mark.parametrize("n,m,r", [(130, 84, 5), (256, 400, 50), (1000, 500, 64), (300, 1032, 37),
+                                   (777, 2000, 128), (128, 80, 1)])
+def test_residual_i8_matches_fp64(n, m, r):
+    """0.5 ||X - G F||^2 with G F on the int8 tensor cores from 8-bit slices:
+    exact products, so the result tracks fp64 at a near-exact fit too."""
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    rng = np.random.default_rng(n + m + r)
+    G = rng.exponential(size=(n, r)).astype(np.float32)
+    F = rng.exponential(size=(r, m)).astype(np.float32)
+    G[rng.uniform(size=G.shape) < 0.2] = 0.0
+    GF = G.astype(np.float64) @ F.astype(np.float64)
+    # a near-exact fit: |X - G F| ~ 1e-3 |X|, the regime where a biased G F fails
+    X = (GF * (1.0 + 1e-3 * rng.normal(size=GF.shape))).astype(np.float32)
+    Gsl = _slices(G)
+    Fsl = _slices(np.ascontiguousarray(F.T))
+    x = torch.from_numpy(X).to(dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    ws = torch.empty((L.lib().nmfb_residual_i8_workspace_bytes() // 8 + 1,), dtype=torch.float64,
+                     device=dev)
+    L.call("nmfb_residual_i8", D.vp(x), n, m, D.vp(Gsl), D.vp(Fsl), r, D.vp(out), D.vp(ws),
+           D.stream_handle())
+    want = 0.5 * np.sum((X.astype(np.float64) - GF) ** 2)
+    got = float(out.item())
+    assert abs(got - want) / want < 2e-5, (got, want)
