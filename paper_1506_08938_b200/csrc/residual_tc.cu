@@ -131,16 +131,6 @@ __device__ __forceinline__ void umma_i8_elect(uint32_t d, uint64_t a, uint64_t b
         "}\n" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void umma_commit_elect(uint64_t *bar) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-        "}\n" ::"r"(smem_u32(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),

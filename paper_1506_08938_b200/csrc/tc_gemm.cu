@@ -18,6 +18,7 @@
 //   warps 2-5  A_lo split during the main loop, then the TMEM -> global epilogue
 // HBM roofline: bytes = 4*M*K (A, streamed once) + B tiles (L2-resident) + C.
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -535,34 +536,118 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
 // TMEM: two 256-column chunk buffers.
 // ---------------------------------------------------------------------------
 constexpr int TC3_BM = 256;  // X rows per tile (MMA N)
+// tuning aid (NMFB_TC_DEBUG=64): CTA 0 per-k-block timeline
+__device__ long long g_tc3_dbg[5][256];
+__device__ long long g_tc3_cta[2][160];  // per-CTA start / end (NMFB_TC_DEBUG=64)
+__device__ __forceinline__ long long gtime_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 constexpr int TC3_THREADS = 512;
-constexpr int TC3_NS = 3;    // TMA stages (X + F')
-constexpr int TC3_NL = 2;    // X_lo buffers
+constexpr int TC3_NX = 4;    // X stages (32 KB, HBM)
+constexpr int TC3_NF = 2;    // F' stages (16 KB, L2-resident factor)
+constexpr int TC3_NL = 2;    // split buffers (16 KB bf16 X_lo + 8 KB bf16 [F_hi ; 0])
+
+// bf16 correction MMA (kind::f16): D += [bf16(F_hi) ; 0] (M = 128, 64-byte
+// K rows, SWIZZLE_64B) x bf16(X_lo)^T (N = 256).  X_lo ~ 2^-10 |X|, so bf16
+// (8-bit, round-to-nearest) costs ~2^-19 of a term, unbiased -- far below the
+// 3xTF32 target -- and halves the X_lo smem footprint and MMA count.
+__device__ __forceinline__ uint64_t desc_sw64(const void *p) {
+    uint64_t d = (uint64_t)((smem_u32(p) & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;  // 8 rows x 64 B
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;           // SWIZZLE_64B
+    return d;
+}
+__device__ __forceinline__ void umma_bf16_elect(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                                uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, 1, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc));
+}
+// 8 fp32 (two 16-byte chunks) -> x - tf32(x) rounded to bf16, packed
+__device__ __forceinline__ uint4 lo_bf16x8(float4 a, float4 b) {
+    auto lo = [](float v) { return v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); };
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(lo(a.x), lo(a.y));
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(lo(a.z), lo(a.w));
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(lo(b.x), lo(b.y));
+    __nv_bfloat162 p3 = __floats2bfloat162_rn(lo(b.z), lo(b.w));
+    return make_uint4(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1),
+                      *reinterpret_cast<uint32_t *>(&p2), *reinterpret_cast<uint32_t *>(&p3));
+}
+__device__ __forceinline__ uint4 bf16x8(float4 a, float4 b) {
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(a.x, a.y);
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(a.z, a.w);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(b.x, b.y);
+    __nv_bfloat162 p3 = __floats2bfloat162_rn(b.z, b.w);
+    return make_uint4(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1),
+                      *reinterpret_cast<uint32_t *>(&p2), *reinterpret_cast<uint32_t *>(&p3));
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
 
 __global__ void __launch_bounds__(TC3_THREADS, 1)
     tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmBlo, float *__restrict__ C, int M, int N,
                     const TcSched sched, int chunk_kb, int64_t slot_stride, int dbg) {
-    constexpr int NS = TC3_NS, NL = TC3_NL;
+    // separate rings: X (HBM, ~2 us TMA latency under load -> deep), F' (L2,
+    // shallow) and the split products [X_lo bf16 | F_hi bf16]
+    constexpr int NX = TC3_NX, NF = TC3_NF, NL = TC3_NL;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    constexpr uint32_t x_bytes = TC3_BM * TC_BK * 4;   // 32 KB
+    constexpr uint32_t x_bytes = TC3_BM * TC_BK * 4;   // 32 KB fp32 X tile
     constexpr uint32_t f_bytes = 128 * TC_BK * 4;      // 16 KB ([hi ; lo] 64 + 64 rows)
-    constexpr uint32_t stage_bytes = x_bytes + f_bytes;
-    uint8_t *xlo = smem + (size_t)NS * stage_bytes;
-    uint64_t *bars = (uint64_t *)(xlo + (size_t)NL * x_bytes);
-    uint64_t *full = bars, *empty = bars + NS;
-    uint64_t *xlo_full = bars + 2 * NS, *xlo_free = bars + 2 * NS + NL;
-    uint64_t *tmem_full = bars + 2 * NS + 2 * NL, *tmem_empty = tmem_full + 2;
+    constexpr uint32_t xl_bytes = TC3_BM * TC_BK * 2;  // 16 KB bf16 X_lo
+    constexpr uint32_t fb_bytes = 128 * TC_BK * 2;     // 8 KB bf16 [F_hi ; 0]
+    constexpr uint32_t l_bytes = xl_bytes + fb_bytes;
+    uint8_t *xr = smem;
+    uint8_t *fr = xr + (size_t)NX * x_bytes;
+    uint8_t *lr = fr + (size_t)NF * f_bytes;
+    uint64_t *bars = (uint64_t *)(lr + (size_t)NL * l_bytes);
+    uint64_t *xfull = bars, *xempty = xfull + NX;
+    uint64_t *ffull = xempty + NX, *fempty = ffull + NF;
+    uint64_t *xlo_full = fempty + NF, *xlo_free = xlo_full + NL;
+    uint64_t *tmem_full = xlo_free + NL, *tmem_empty = tmem_full + 2;
     uint32_t *tmem_slot = (uint32_t *)(tmem_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if ((dbg & 64) && threadIdx.x == 0 && blockIdx.x < 160) g_tc3_cta[0][blockIdx.x] = gtime_ns();
+    // rows 64..127 of the bf16 F_hi operands stay zero
+    for (int q = threadIdx.x; q < NL * (int)(fb_bytes / 2) / 16; q += TC3_THREADS) {
+        const int j = q / (int)(fb_bytes / 2 / 16), w = q % (int)(fb_bytes / 2 / 16);
+        *reinterpret_cast<uint4 *>(lr + (size_t)j * l_bytes + xl_bytes + fb_bytes / 2 + w * 16) =
+            make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int s = 0; s < NS; ++s) {
-                mbar_init(&full[s], 1);
-                mbar_init(&empty[s], 1);
+            // X / F' stages are free once the main MMAs (commit) and the split
+            // warps (128 arrivals) are done with them -- not after the X_lo MMAs
+            for (int s = 0; s < NX; ++s) {
+                mbar_init(&xfull[s], 1);
+                mbar_init(&xempty[s], 1 + 128);
+            }
+            for (int s = 0; s < NF; ++s) {
+                mbar_init(&ffull[s], 1);
+                mbar_init(&fempty[s], 1 + 128);
             }
             for (int j = 0; j < NL; ++j) {
                 mbar_init(&xlo_full[j], 128);
@@ -592,94 +677,111 @@ __global__ void __launch_bounds__(TC3_THREADS, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     }
     if (warp == 0) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            int i = 0;
-            for_each_segment(sched, blockIdx.x, [&](int tile, int kb0, int nkb, int, bool) {
-                for (int t = 0; t < nkb; ++t, ++i) {
-                    const int s = i % NS;
-                    mbar_wait(&empty[s], ((uint32_t)(i / NS) & 1u) ^ 1u);
-                    uint8_t *st = smem + (size_t)s * stage_bytes;
-                    mbar_expect_tx(&full[s], stage_bytes);
-                    const int kc = (kb0 + t) * TC_BK;
-                    tma_load_2d(&tmX, &full[s], st, kc, tile * TC3_BM);
-                    tma_load_2d(&tmB, &full[s], st + x_bytes, kc, 0);
-                    tma_load_2d(&tmBlo, &full[s], st + x_bytes + f_bytes / 2, kc, 0);
-                }
-            });
-        }
+        // ---------------- TMA producer (converged warp, elected issue) ----------------
+        int i = 0;
+        for_each_segment(sched, blockIdx.x, [&](int tile, int kb0, int nkb, int, bool) {
+            for (int t = 0; t < nkb; ++t, ++i) {
+                const int sx = i % NX, sf = i % NF;
+                const int kc = (kb0 + t) * TC_BK;
+                mbar_wait(&xempty[sx], ((uint32_t)(i / NX) & 1u) ^ 1u);
+                mbar_expect_tx_elect(&xfull[sx], x_bytes);
+                tma_load_2d_elect(&tmX, &xfull[sx], xr + (size_t)sx * x_bytes, kc, tile * TC3_BM);
+                if ((dbg & 64) && blockIdx.x == 0 && i < 256 && lane == 0) g_tc3_dbg[0][i] = gtime_ns();
+                mbar_wait(&fempty[sf], ((uint32_t)(i / NF) & 1u) ^ 1u);
+                mbar_expect_tx_elect(&ffull[sf], f_bytes);
+                uint8_t *fs = fr + (size_t)sf * f_bytes;
+                tma_load_2d_elect(&tmB, &ffull[sf], fs, kc, 0);
+                tma_load_2d_elect(&tmBlo, &ffull[sf], fs + f_bytes / 2, kc, 0);
+            }
+        });
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
+        // ---------------- MMA issuer (converged warp, elected issue) ----------------
         constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
                                    ((uint32_t)(TC3_BM >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        if (lane == 0) {
-            int i = 0, g = 0;
-            for_each_segment(sched, blockIdx.x, [&](int, int, int nkb, int, bool) {
-                for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++g) {
-                    const int buf = g & 1;
-                    mbar_wait(&tmem_empty[buf], ((uint32_t)(g >> 1) & 1u) ^ 1u);
+        constexpr uint32_t idesc_bf = (1u << 4) | (1u << 7) | (1u << 10) |
+                                      ((uint32_t)(TC3_BM >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        int i = 0, g = 0;
+        for_each_segment(sched, blockIdx.x, [&](int, int, int nkb, int, bool) {
+            for (int c0 = 0; c0 < nkb; c0 += chunk_kb, ++g) {
+                const int buf = g & 1;
+                mbar_wait(&tmem_empty[buf], ((uint32_t)(g >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t d = tmem + (uint32_t)(buf * TC3_BM);
+                const int c1 = min(nkb, c0 + chunk_kb);
+                for (int t = c0; t < c1; ++t, ++i) {
+                    const int sx = i % NX, sf = i % NF, j = i % NL;
+                    const uint64_t fa = umma_desc_sw128(fr + (size_t)sf * f_bytes);
+                    const uint64_t xb = umma_desc_sw128(xr + (size_t)sx * x_bytes);
+                    const uint64_t xl = desc_sw64(lr + (size_t)j * l_bytes);
+                    const uint64_t fbd = desc_sw64(lr + (size_t)j * l_bytes + xl_bytes);
+                    mbar_wait(&ffull[sf], (uint32_t)(i / NF) & 1u);
+                    mbar_wait(&xfull[sx], (uint32_t)(i / NX) & 1u);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t d = tmem + (uint32_t)(buf * TC3_BM);
-                    const int c1 = min(nkb, c0 + chunk_kb);
-                    for (int t = c0; t < c1; ++t, ++i) {
-                        const int s = i % NS, j = i % NL;
-                        uint8_t *st = smem + (size_t)s * stage_bytes;
-                        const uint64_t fa = umma_desc_sw128(st + x_bytes);
-                        const uint64_t xb = umma_desc_sw128(st);
-                        const uint64_t xl = umma_desc_sw128(xlo + (size_t)j * x_bytes);
-                        mbar_wait(&full[s], (uint32_t)(i / NS) & 1u);
-                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if ((dbg & 64) && blockIdx.x == 0 && i < 256 && lane == 0) g_tc3_dbg[1][i] = gtime_ns();
 #pragma unroll
-                        for (int k = 0; k < TC_BK / 8; ++k) {
-                            const uint64_t dk = (uint64_t)((k * 32) >> 4);
-                            umma_tf32(d, fa + dk, xb + dk, idesc, (t > c0 || k > 0) ? 1u : 0u);
-                        }
-                        mbar_wait(&xlo_full[j], (uint32_t)(i / NL) & 1u);
-                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                        if (!(dbg & 4)) {
-#pragma unroll
-                            for (int k = 0; k < TC_BK / 8; ++k) {
-                                const uint64_t dk = (uint64_t)((k * 32) >> 4);
-                                umma_tf32(d, fa + dk, xl + dk, idesc, 1u);
-                            }
-                        }
-                        umma_commit(&empty[s]);
-                        umma_commit(&xlo_free[j]);
+                    for (int k = 0; k < TC_BK / 8; ++k) {
+                        const uint64_t dk = (uint64_t)((k * 32) >> 4);
+                        umma_tf32_elect(d, fa + dk, xb + dk, idesc, (t > c0 || k > 0) ? 1u : 0u);
                     }
-                    umma_commit(&tmem_full[buf]);
+                    umma_commit_elect(&xempty[sx]);
+                    umma_commit_elect(&fempty[sf]);
+                    mbar_wait(&xlo_full[j], (uint32_t)(i / NL) & 1u);
+                    if ((dbg & 64) && blockIdx.x == 0 && i < 256 && lane == 0) g_tc3_dbg[2][i] = gtime_ns();
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (!(dbg & 4)) {
+#pragma unroll
+                        for (int k = 0; k < TC_BK / 16; ++k) {
+                            const uint64_t dk = (uint64_t)((k * 32) >> 4);  // 16 bf16 = 32 B
+                            umma_bf16_elect(d, fbd + dk, xl + dk, idesc_bf);
+                        }
+                    }
+                    umma_commit_elect(&xlo_free[j]);
+                    if ((dbg & 64) && blockIdx.x == 0 && i < 256 && lane == 0) g_tc3_dbg[3][i] = gtime_ns();
                 }
-            });
-        }
+                umma_commit_elect(&tmem_full[buf]);
+            }
+        });
         __syncwarp();
     } else if (warp >= 4 && warp < 8) {
-        // ------- split warps: X_lo = X - tf32(X), same swizzled layout -------
+        // ------- split warps: bf16(X - tf32(X)) and bf16(F_hi) into the L ring -------
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
         const int t128 = threadIdx.x - 128;
         int i = 0;
         for_each_segment(sched, blockIdx.x, [&](int, int, int nkb, int, bool) {
             for (int t = 0; t < nkb; ++t, ++i) {
-                const int s = i % NS, j = i % NL;
-                mbar_wait(&full[s], (uint32_t)(i / NS) & 1u);
+                const int sx = i % NX, sf = i % NF, j = i % NL;
+                mbar_wait(&xfull[sx], (uint32_t)(i / NX) & 1u);
+                mbar_wait(&ffull[sf], (uint32_t)(i / NF) & 1u);
                 mbar_wait(&xlo_free[j], ((uint32_t)(i / NL) & 1u) ^ 1u);
-                const uint32_t src = smem_u32(smem + (size_t)s * stage_bytes);
-                const uint32_t dst = smem_u32(xlo + (size_t)j * x_bytes);
-#pragma unroll 4
-                for (int q = 0; q < ((dbg & 2) ? 0 : (int)(x_bytes / 16 / 128)); ++q) {
-                    const uint32_t off = (uint32_t)(q * 128 + t128) * 16u;
-                    float4 v;
-                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                                 : "r"(src + off));
-                    v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(dst + off),
-                                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                                 : "memory");
+                if ((dbg & 64) && blockIdx.x == 0 && i < 256 && threadIdx.x == 128) g_tc3_dbg[4][i] = gtime_ns();
+                const uint32_t xsrc = smem_u32(xr + (size_t)sx * x_bytes);
+                const uint32_t fsrc = smem_u32(fr + (size_t)sf * f_bytes);
+                const uint32_t ldst = smem_u32(lr + (size_t)j * l_bytes);
+                // items (row r, bf16 chunk cb): fp32 chunks 2cb, 2cb+1 of a SW128
+                // row (chunk c at r*128 + ((c ^ (r & 7)) << 4)) -> one SW64 chunk
+                // (chunk c at r*64 + ((c ^ ((r >> 1) & 3)) << 4))
+#pragma unroll 2
+                for (int q = t128; q < ((dbg & 2) ? 0 : TC3_BM * 4); q += 128) {
+                    const int r = q >> 2, cb = q & 3;
+                    const uint32_t rb = xsrc + (uint32_t)r * 128u;
+                    const float4 a = lds128(rb + ((uint32_t)((2 * cb) ^ (r & 7)) << 4));
+                    const float4 b = lds128(rb + ((uint32_t)((2 * cb + 1) ^ (r & 7)) << 4));
+                    sts128(ldst + (uint32_t)r * 64u + ((uint32_t)(cb ^ ((r >> 1) & 3)) << 4),
+                           lo_bf16x8(a, b));
+                }
+                for (int q = t128; q < ((dbg & 2) ? 0 : 64 * 4); q += 128) {
+                    const int r = q >> 2, cb = q & 3;
+                    const uint32_t rb = fsrc + (uint32_t)r * 128u;
+                    const float4 a = lds128(rb + ((uint32_t)((2 * cb) ^ (r & 7)) << 4));
+                    const float4 b = lds128(rb + ((uint32_t)((2 * cb + 1) ^ (r & 7)) << 4));
+                    sts128(ldst + xl_bytes + (uint32_t)r * 64u +
+                               ((uint32_t)(cb ^ ((r >> 1) & 3)) << 4),
+                           bf16x8(a, b));
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&xlo_full[j]);
+                mbar_arrive(&xempty[sx]);
+                mbar_arrive(&fempty[sf]);
             }
         });
     } else if (warp >= 8) {
@@ -734,6 +836,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1)
             }
         });
     }
+    if ((dbg & 64) && warp == 8 && lane == 0 && blockIdx.x < 160) g_tc3_cta[1][blockIdx.x] = gtime_ns();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) {
@@ -869,8 +972,8 @@ int tc_parts(int64_t M, int64_t K, int N, int splits) {
 static void launch_tc3(const CUtensorMap &tx, const CUtensorMap &tb, const CUtensorMap &tbl,
                        float *C, int M, int N, const TcSched &s, int chunk_kb, cudaStream_t st) {
     static bool attr = false;
-    const size_t smem = (size_t)TC3_NS * (TC3_BM + 128) * TC_BK * 4 +
-                        (size_t)TC3_NL * TC3_BM * TC_BK * 4 + 256 + 1024;
+    const size_t smem = (size_t)TC3_NX * TC3_BM * TC_BK * 4 + (size_t)TC3_NF * 128 * TC_BK * 4 +
+                        (size_t)TC3_NL * (TC3_BM + 128) * TC_BK * 2 + 256 + 1024;
     if (!attr) {
         cudaFuncSetAttribute(tc_gemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -901,6 +1004,13 @@ static void launch_tc2(const CUtensorMap &ta, const CUtensorMap &tb, const CUten
     static const int dbg = getenv("NMFB_TC_DEBUG") ? atoi(getenv("NMFB_TC_DEBUG")) : 0;
     tc_gemm2_kernel<BN><<<s.G, TC2_THREADS, smem, st>>>(ta, tb, tbl, C, M, N, s, ns, chunk_kb,
                                                         (int64_t)M * N, dbg);
+}
+
+extern "C" int nmfb_debug_tc3_timeline(long long *host_out) {
+    return cudaMemcpyFromSymbol(host_out, g_tc3_dbg, sizeof(g_tc3_dbg)) == cudaSuccess ? 0 : 3;
+}
+extern "C" int nmfb_debug_tc3_cta(long long *host_out) {
+    return cudaMemcpyFromSymbol(host_out, g_tc3_cta, sizeof(g_tc3_cta)) == cudaSuccess ? 0 : 3;
 }
 
 int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
