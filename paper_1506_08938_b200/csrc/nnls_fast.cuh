@@ -252,15 +252,12 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                     }
                 }
             }
-            // greedy coordinate descent: ra selections, the chosen coordinate's
-            // gradient column update fused into the next scan (kernels.py:104-132).
-            // Closed-form step dx = max(y - g, 0) - y = -min(g, y); decrease
-            // |g dx + dx^2 / 2| = |dx (g + dx / 2)|; ties -> lowest index.
+            constexpr int IB = (R <= 128) ? 7 : 8;
+            constexpr unsigned IMASK = (1u << IB) - 1u;
             int pp = -1;
             float pdx = 0.f;
             for (int s = 0; s < ra; ++s) {
-                float best = 0.f, bdx = 0.f;
-                int bp = INT_MAX;
+                unsigned key[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const int k = e * L + l;
@@ -268,44 +265,39 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                     if (pp >= 0) {
                         gi = fmaf(Qrow[e * L * S + pp], pdx, gi);
                         gr[e] = gi;
-                        if (k == pp) y[e] += pdx;
                     }
                     const float dxi = -fminf(gi, y[e]);
-                    const float dec = fabsf(dxi * fmaf(0.5f, dxi, gi));
-                    if (dec > best) {
-                        best = dec;
-                        bp = k;
-                        bdx = dxi;
-                    }
+                    const float dec = dxi * fmaf(0.5f, dxi, gi);
+                    key[e] = (__float_as_uint(dec) & (0x7FFFFFFFu & ~IMASK)) | (IMASK - (unsigned)k);
                 }
-                if (L > 1) {
-                    const int mine = bp;
 #pragma unroll
-                    for (int o = L / 2; o > 0; o >>= 1) {
-                        const float ob = __shfl_xor_sync(gmask, best, o, L);
-                        const int op = __shfl_xor_sync(gmask, bp, o, L);
-                        if (ob > best || (ob == best && op < bp)) {
-                            best = ob;
-                            bp = op;
-                        }
-                    }
-                    // step of the winner, broadcast from the lane that owns it
-                    const float wdx = (bp == mine) ? bdx : 0.f;
-                    bdx = __shfl_sync(gmask, wdx, (bp == INT_MAX) ? 0 : (bp % L), L);
-                }
-                if (!(best > 0.f)) {
+                for (int w = 1; w < E; w <<= 1)
+#pragma unroll
+                    for (int e = 0; e + w < E; e += 2 * w) key[e] = max(key[e], key[e + w]);
+                unsigned kb = key[0];
+#pragma unroll
+                for (int o = L / 2; o > 0; o >>= 1) kb = max(kb, __shfl_xor_sync(gmask, kb, o, L));
+                if ((kb & ~IMASK) == 0u) {
                     pp = -1;
                     break;
                 }
+                const int p = (int)(IMASK - (kb & IMASK));
+                float dxo = 0.f;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if (e * L + l == p) {
+                        dxo = -fminf(gr[e], y[e]);
+                        y[e] += dxo;
+                    }
+                }
                 moved = true;
-                pp = bp;
-                pdx = bdx;
+                pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, p % L, L);
+                pp = p;
             }
             if (pp >= 0) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     gr[e] = fmaf(Qrow[e * L * S + pp], pdx, gr[e]);
-                    if (e * L + l == pp) y[e] += pdx;
                 }
             }
             iters += 1;
