@@ -126,16 +126,20 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    --set full summary (profiles/ncu_summary.json), or None."""
-    path = os.path.join(REPO, "profiles", "ncu_summary.json")
-    if not os.path.exists(path):
+def profile_traffic(kernel="nmfb_tc_gemm"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/traffic_r*.json, newest
+    round), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "traffic_r*.json")))
+    if not files:
         return None
     try:
-        with open(path) as f:
-            return json.load(f).get("gemm_tall", {}).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
+        with open(files[-1]) as f:
+            k = json.load(f).get(kernel)
+        return None if k is None else int(k["dram_bytes_read"]) + int(k["dram_bytes_write"])
+    except (OSError, ValueError, KeyError, TypeError):
         return None
 
 
