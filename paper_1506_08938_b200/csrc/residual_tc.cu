@@ -12,9 +12,10 @@
 //   A0 = g0.f0,  A1 = g0.f1 + g1.f0,  A2 = g0.f2 + g1.f1 + g2.f0
 //
 // Six u8 x u8 -> s32 products (tcgen05.mma kind::i8, exact), one TMEM
-// accumulator per order.  The epilogue combines the orders in fp32 (two
-// round-to-nearest adds: unbiased), subtracts from the X tile, squares in fp32
-// and sums in fp64.  Accuracy ~2^-24 relative on G F, unbiased -- at least as
+// accumulator per order.  The epilogue combines the orders into one unsigned
+// integer (2^8 A0 + A1 + round(2^-8 A2) < 2^32), converts it once
+// (round-to-nearest: unbiased), subtracts from the X tile, squares in fp32 and
+// sums in fp64.  Accuracy ~2^-24 relative on G F, unbiased -- at least as
 // good as an fp32 FFMA dot product, at tensor-core speed.
 //
 // Persistent kernel, one CTA per SM, tiles of 128 rows (i, n-dim) x 80
@@ -26,12 +27,13 @@
 //   warp 1     MMA: 6 products x ceil(r/32) k-steps into the tile's 3
 //              accumulators (2 x 3 x 80 = 480 TMEM columns, double-buffered)
 //   warps 4-23 epilogue: TMEM lanes = rows of the tile, five warps per lane
-//              quarter (16 columns each, released to the MMA warp as soon as
-//              they are in registers); int -> float by the 2^23 magic
-//              number and packed FP32x2 math (~4 instructions per element)
-// Bound: TMEM reads (12 B per element at 64 B/clk/SM) ~ HBM reads of X
-// (4 B per element) ~ 0.13 ms per 2e8 elements; the FFMA kernel needs 2r
-// flops per element (0.27 ms at the fp32 peak for r = 50).
+//              quarter (16 columns each); the three orders are combined in
+//              integer arithmetic, converted once, and consumed with packed
+//              FP32x2 math
+// Bound: HBM reads of X (4 B per element, 0.12 ms per 2e8 elements at the
+// measured peak) against ~93 ns per u8 MMA (12 per 128 x 80 tile) and the
+// epilogue's issue rate; the FFMA kernel needs 2r flops per element
+// (0.27 ms at the fp32 peak for r = 50).
 #include <cuda.h>
 
 #include <algorithm>
@@ -48,8 +50,8 @@ constexpr int RQ_BM = 128;     // rows of X per tile (TMEM lanes)
 constexpr int RQ_BN = 80;      // columns of X per tile (MMA N)
 constexpr int RQ_XLD = 84;     // smem row pitch of the X tile (floats)
 constexpr int RQ_KB = 128;     // max bytes per slice row (r <= 128); 64 when r <= 64
-constexpr int RQ_CW = 8;         // epilogue chunk (columns per TMEM load)
-constexpr int RQ_EPW = 5;        // epilogue warps per TMEM lane quarter (2 chunks each)
+constexpr int RQ_CW = 16;        // epilogue columns per warp (one x16 TMEM load per order)
+constexpr int RQ_EPW = RQ_BN / RQ_CW;  // epilogue warps per TMEM lane quarter (5)
 constexpr int RQ_EPI = 128 * RQ_EPW;  // epilogue threads
 constexpr int RQ_THREADS = 128 + RQ_EPI;  // TMA, MMA, 2 idle, epilogue warps
 
@@ -304,10 +306,6 @@ __global__ void __launch_bounds__(RQ_THREADS, 1)
         const int cpart = (warp - 4) >> 2;  // column chunks c = cpart (mod RQ_EPW)
         const int row_in_tile = quarter * 32 + lane;
         const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-        const uint32_t M23 = 0x4B000000u;  // 2^23: (v | M23) as float = 2^23 + v, v < 2^23
-        const float2 c23 = make_float2(-8388608.f, -8388608.f);
-        const float2 k7 = make_float2(1.f / 128.f, 1.f / 128.f);
-        const float2 k8 = make_float2(1.f / 256.f, 1.f / 256.f);
         double total = 0.0;
         for (int64_t t = t0; t < t1; ++t) {
             const int it = (int)(t - t0), s = it & 1, sx = it % NX, sf_ = it % NF;
@@ -315,7 +313,8 @@ __global__ void __launch_bounds__(RQ_THREADS, 1)
             const int64_t i = (int64_t)rb * RQ_BM + row_in_tile;
             const int64_t j0 = (int64_t)ct * RQ_BN;
             const bool row_ok = i < n;
-            const float si = row_ok ? sg[i] * (1.f / 65536.f) : 0.f;
+            const float si = row_ok ? sg[i] * (1.f / 16777216.f) : 0.f;
+            const float2 nsi = make_float2(-si, -si);
             // this warp's column scales, fetched before the waits (latency hidden);
             // columns past m get scale 0 so their (garbage) G F drops out
             float4 sfr[RQ_BN / RQ_CW / RQ_EPW][RQ_CW / 4];
@@ -342,45 +341,34 @@ __global__ void __launch_bounds__(RQ_THREADS, 1)
             const float *xrow = xs + sx * (x_bytes / 4) + row_in_tile * RQ_XLD;
             const uint32_t base = tmem + lane_base + (uint32_t)(s * 3 * RQ_BN);
             float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int c = cpart; c < ((dbg & 1) ? 0 : RQ_BN / RQ_CW); c += RQ_EPW) {
-                const int c0 = RQ_CW * c;
+            if (!(dbg & 1)) {
+                // this warp's 16 columns; U = 2^8 A0 + A1 + round(2^-8 A2) is an
+                // unsigned integer < 2^32 (A0 <= 32 ks 255^2), converted once with
+                // round-to-nearest (relative 2^-24, unbiased): G F = s_i t_j 2^-24 U
+                const int c0 = RQ_CW * cpart;
                 uint32_t a0[RQ_CW], a1[RQ_CW], a2[RQ_CW];
-                tmem_ld8(base + (uint32_t)c0, a0);
-                tmem_ld8(base + (uint32_t)(RQ_BN + c0), a1);
-                tmem_ld8(base + (uint32_t)(2 * RQ_BN + c0), a2);
-                float4 xq[RQ_CW / 4], fq[RQ_CW / 4];
+                tmem_ld16(base + (uint32_t)c0, a0);
+                tmem_ld16(base + (uint32_t)(RQ_BN + c0), a1);
+                tmem_ld16(base + (uint32_t)(2 * RQ_BN + c0), a2);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float u[RQ_CW];
+#pragma unroll
+                for (int q = 0; q < RQ_CW; ++q)
+                    u[q] = __uint2float_rn((a0[q] << 8) + a1[q] + ((a2[q] + 128u) >> 8));
+                const float4 *sfq = sfr[0];
 #pragma unroll
                 for (int q = 0; q < RQ_CW / 4; ++q) {
-                    xq[q] = *reinterpret_cast<const float4 *>(xrow + c0 + 4 * q);
-                    fq[q] = sfr[(c - cpart) / RQ_EPW][q];
-                }
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int p = 0; p < RQ_CW / 2; ++p) {
-                    const int e = 2 * p;
-                    const float4 &x4 = xq[p >> 1];
-                    const float4 &f4 = fq[p >> 1];
-                    const float2 xv = (p & 1) ? make_float2(x4.z, x4.w) : make_float2(x4.x, x4.y);
-                    const float2 sv = (p & 1) ? make_float2(-si * f4.z, -si * f4.w)
-                                              : make_float2(-si * f4.x, -si * f4.y);
-                    // exact int -> float via the 2^23 magic number; A2 (< 3 r 255^2)
-                    // may exceed 2^23, so it is halved with rounding (its weight is
-                    // 2^-16: the lost bit is 2^-41 relative)
-                    const float2 u0 = make_float2(__uint_as_float(a0[e] | M23),
-                                                  __uint_as_float(a0[e + 1] | M23));
-                    const float2 u1 = make_float2(__uint_as_float(a1[e] | M23),
-                                                  __uint_as_float(a1[e + 1] | M23));
-                    const float2 u2 = make_float2(__uint_as_float(((a2[e] + 1u) >> 1) | M23),
-                                                  __uint_as_float(((a2[e + 1] + 1u) >> 1) | M23));
-                    const float2 f0 = __fadd2_rn(u0, c23);  // A0   (exact)
-                    const float2 f1 = __fadd2_rn(u1, c23);  // A1   (exact)
-                    const float2 f2 = __fadd2_rn(u2, c23);  // A2/2 (exact)
-                    // A0 + 2^-8 (A1 + 2^-7 (A2 / 2)): two round-to-nearest steps
-                    const float2 lo = __ffma2_rn(f2, k7, f1);
-                    const float2 sum = __ffma2_rn(lo, k8, f0);
-                    const float2 d = __ffma2_rn(sum, sv, xv);  // X - G F, one rounding
-                    acc = __ffma2_rn(d, d, acc);
+                    const float4 x4 = *reinterpret_cast<const float4 *>(xrow + c0 + 4 * q);
+                    const float4 f4 = sfq[q];
+                    const float2 s0 = __fmul2_rn(nsi, make_float2(f4.x, f4.y));
+                    const float2 s1 = __fmul2_rn(nsi, make_float2(f4.z, f4.w));
+                    // X - G F with one rounding, squared into the running sum
+                    const float2 d0 = __ffma2_rn(make_float2(u[4 * q], u[4 * q + 1]), s0,
+                                                 make_float2(x4.x, x4.y));
+                    const float2 d1 = __ffma2_rn(make_float2(u[4 * q + 2], u[4 * q + 3]), s1,
+                                                 make_float2(x4.z, x4.w));
+                    acc = __ffma2_rn(d0, d0, acc);
+                    acc = __ffma2_rn(d1, d1, acc);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
