@@ -209,7 +209,20 @@ class CudaEngine:
         p = self.pieces
         p.zero_()
         G = st.G[lo:hi]
-        if d.kind == "dense":
+        if d.kind == "dense" and getattr(st, "use_i8", False):
+            # exact int8 tensor-core residual over my column block (the same
+            # kernel as the single-GPU path): 8-bit slices of the full G and of
+            # my rows of F^T, X block (n x m_local) row-major
+            q = k % 2
+            L.call("nmfb_slice_u8", D.vp(st.G), d.n, self.r, self.r, D.vp(st.Gsl[q]),
+                   D.stream_handle())
+            L.call("nmfb_slice_u8", D.vp(st.FT), d.m, self.r, self.r, D.vp(st.Fsl[q]),
+                   D.stream_handle())
+            L.call("nmfb_residual_i8", D.vp(d.X), d.n, d.m, D.vp(st.Gsl[q]), D.vp(st.Fsl[q]),
+                   self.r, D.vp(p[0:1]), D.vp(st.rq_ws), D.stream_handle())
+            if (cfg.beta1 or cfg.beta2) and hi > lo:
+                st.dot(G, st.code, None, L.F64, (hi - lo) * self.r, p[1:4])
+        elif d.kind == "dense":
             L.call("nmfb_dense_residual", st.code, D.vp(d.XT), d.m, d.n, D.vp(st.G),
                    D.vp(st.FT), self.r, D.vp(p[0:1]), D.vp(st.res_ws), D.stream_handle())
             if (cfg.beta1 or cfg.beta2) and hi > lo:
