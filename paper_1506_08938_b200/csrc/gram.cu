@@ -154,19 +154,22 @@ int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, doub
 // H = G + diag_add * I, compacted to the active dims (parallel.py:87-91).
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(256) rescale_kernel(const double *__restrict__ G, int r,
-                                                      double diag_add, T *Qa, T *scale_a,
-                                                      int32_t *act_idx, uint8_t *active,
-                                                      int32_t *ra_dev, double *full_scale) {
+__global__ void __launch_bounds__(1024) rescale_kernel(const double *__restrict__ G, int r,
+                                                       double diag_add, T *Qa, T *scale_a,
+                                                       int32_t *act_idx, uint8_t *active,
+                                                       int32_t *ra_dev, double *full_scale) {
     extern __shared__ double sh[];
     double *diag = sh;                         // r
-    int *pos = (int *)(sh + r);                // r: compact position or -1
+    double *sq = sh + r;                       // r: sqrt(diag)
+    int *pos = (int *)(sh + 2 * r);            // r: compact position or -1
     __shared__ double s_delta;
     __shared__ int s_ra;
     const int tid = threadIdx.x;
     for (int i = tid; i < r; i += blockDim.x) {
         // H = Q_g + (2.0 * mu2) * np.eye(r): the identity term adds diag_add * 1.0
-        diag[i] = __dadd_rn(G[i * r + i], __dmul_rn(diag_add, 1.0));
+        const double d = __dadd_rn(G[i * r + i], __dmul_rn(diag_add, 1.0));
+        diag[i] = d;
+        sq[i] = __dsqrt_rn(d);
     }
     __syncthreads();
     if (tid == 0) {
@@ -192,9 +195,8 @@ __global__ void __launch_bounds__(256) rescale_kernel(const double *__restrict__
     __syncthreads();
     const int ra = s_ra;
     for (int i = tid; i < r; i += blockDim.x) {
-        double sc = __dsqrt_rn(diag[i]);
-        if (full_scale) full_scale[i] = sc;
-        if (pos[i] >= 0) scale_a[pos[i]] = (T)sc;
+        if (full_scale) full_scale[i] = sq[i];
+        if (pos[i] >= 0) scale_a[pos[i]] = (T)sq[i];
     }
     for (int idx = tid; idx < r * r; idx += blockDim.x) {
         int i = idx / r, j = idx % r;
@@ -204,9 +206,8 @@ __global__ void __launch_bounds__(256) rescale_kernel(const double *__restrict__
         if (i == j) {
             v = 1.0;
         } else {
-            double si = __dsqrt_rn(diag[i]), sj = __dsqrt_rn(diag[j]);
             // off-diagonal of H = G + diag_add * eye: G_ij + 0.0
-            v = __ddiv_rn(__dadd_rn(G[i * r + j], 0.0), __dmul_rn(si, sj));
+            v = __ddiv_rn(__dadd_rn(G[i * r + j], 0.0), __dmul_rn(sq[i], sq[j]));
         }
         Qa[pi * ra + pj] = (T)v;
     }
@@ -216,13 +217,19 @@ int rescale_launch(int dtype, const double *G, int r, double diag_add, void *Qa,
                    int32_t *act_idx, uint8_t *active, int32_t *ra_dev, double *full_scale,
                    cudaStream_t st) {
     if (r <= 0 || r > 4096) return NMFB_ERR_ARG;
-    size_t smem = r * sizeof(double) + r * sizeof(int);
+    size_t smem = 2 * r * sizeof(double) + r * sizeof(int);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(rescale_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(rescale_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    }
     if (dtype == NMFB_F64)
-        rescale_kernel<double><<<1, 256, smem, st>>>(G, r, diag_add, (double *)Qa,
+        rescale_kernel<double><<<1, 1024, smem, st>>>(G, r, diag_add, (double *)Qa,
                                                      (double *)scale_a, act_idx, active, ra_dev,
                                                      full_scale);
     else
-        rescale_kernel<float><<<1, 256, smem, st>>>(G, r, diag_add, (float *)Qa,
+        rescale_kernel<float><<<1, 1024, smem, st>>>(G, r, diag_add, (float *)Qa,
                                                     (float *)scale_a, act_idx, active, ra_dev,
                                                     full_scale);
     return launch_status();

@@ -125,6 +125,98 @@ __global__ void __launch_bounds__(128) csr_yt_kernel(const int64_t *__restrict__
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fast-path gathers with 16-byte vector loads (r % 4 == 0, r <= 128): lane l
+// of the warp owns components 4l..4l+3 of the output row, so each nonzero is
+// one 128-bit L2 load per active lane (r / 4 lanes) instead of ceil(r/32)
+// scalar loads; unrolled 8 deep for memory-level parallelism.  Same
+// per-component summation order as the scalar kernels (nonzeros in order).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) csc_linear_v4_kernel(const int64_t *__restrict__ indptr,
+                                                            const int32_t *__restrict__ rowidx,
+                                                            const float *__restrict__ vals,
+                                                            int64_t col_lo, int64_t col_hi,
+                                                            const float *__restrict__ G, int r,
+                                                            float mu1, float *__restrict__ h) {
+    const int64_t col = col_lo + (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (col >= col_hi) return;
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < (r >> 2);
+    float4 acc = make_float4(mu1, mu1, mu1, mu1);
+    const int64_t p0 = indptr[col], p1 = indptr[col + 1];
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int myrow = 0;
+        float myv = 0.f;
+        if (lane < cnt) {
+            myrow = rowidx[base + lane];
+            myv = vals[base + lane];
+        }
+#pragma unroll 8
+        for (int u = 0; u < cnt; ++u) {
+            const int row = __shfl_sync(NMFB_FULL_MASK, myrow, u);
+            const float v = __shfl_sync(NMFB_FULL_MASK, myv, u);
+            if (act) {
+                const float4 g = __ldg(reinterpret_cast<const float4 *>(G + (int64_t)row * r) + lane);
+                acc.x = fmaf(-g.x, v, acc.x);
+                acc.y = fmaf(-g.y, v, acc.y);
+                acc.z = fmaf(-g.z, v, acc.z);
+                acc.w = fmaf(-g.w, v, acc.w);
+            }
+        }
+    }
+    if (act) reinterpret_cast<float4 *>(h + (col - col_lo) * r)[lane] = acc;
+}
+
+template <typename TY>
+__global__ void __launch_bounds__(128) csr_yt_chunk_v4_kernel(const int64_t *__restrict__ chunks,
+                                                              int64_t nchunks,
+                                                              const int32_t *__restrict__ colidx,
+                                                              const float *__restrict__ vals,
+                                                              const float *__restrict__ FT, int r,
+                                                              TY *__restrict__ YT,
+                                                              TY *__restrict__ part) {
+    const int64_t ch = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (ch >= nchunks) return;
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < (r >> 2);
+    const int64_t row = chunks[ch * 4 + 0], p0 = chunks[ch * 4 + 1], p1 = chunks[ch * 4 + 2];
+    const int64_t slot = chunks[ch * 4 + 3];
+    TY a0 = TY(0), a1 = TY(0), a2 = TY(0), a3 = TY(0);
+    for (int64_t base = p0; base < p1; base += 32) {
+        const int cnt = (int)min((int64_t)32, p1 - base);
+        int mycol = 0;
+        float myv = 0.f;
+        if (lane < cnt) {
+            mycol = colidx[base + lane];
+            myv = vals[base + lane];
+        }
+#pragma unroll 8
+        for (int u = 0; u < cnt; ++u) {
+            const int col = __shfl_sync(NMFB_FULL_MASK, mycol, u);
+            const float v = __shfl_sync(NMFB_FULL_MASK, myv, u);
+            if (act) {
+                const float4 f = __ldg(reinterpret_cast<const float4 *>(FT + (int64_t)col * r) + lane);
+                a0 = fma((TY)f.x, (TY)v, a0);
+                a1 = fma((TY)f.y, (TY)v, a1);
+                a2 = fma((TY)f.z, (TY)v, a2);
+                a3 = fma((TY)f.w, (TY)v, a3);
+            }
+        }
+    }
+    if (act) {
+        TY *out = ((slot < 0) ? (YT + row * r) : (part + slot * r)) + 4 * lane;
+        out[0] = a0;
+        out[1] = a1;
+        out[2] = a2;
+        out[3] = a3;
+    }
+}
+
+static bool v4_ok(int r, const void *a) {
+    return r % 4 == 0 && r <= 128 && ((uintptr_t)a % 16) == 0;
+}
+
 template <typename T, bool EXACT>
 static int csc_linear_dispatch(const int64_t *indptr, const int32_t *rowidx, const void *vals,
                                int64_t lo, int64_t hi, const void *G, int r, double mu1, void *h,
@@ -133,6 +225,11 @@ static int csc_linear_dispatch(const int64_t *indptr, const int32_t *rowidx, con
     const T *v = (const T *)vals;
     const T *g = (const T *)G;
     T *o = (T *)h;
+    if (!EXACT && sizeof(T) == 4 && v4_ok(r, G) && v4_ok(r, h)) {
+        csc_linear_v4_kernel<<<grid, 128, 0, st>>>(indptr, rowidx, (const float *)vals, lo, hi,
+                                                   (const float *)G, r, (float)mu1, (float *)h);
+        return launch_status();
+    }
 #define NMFB_CSC(Cc) \
     csc_linear_kernel<T, EXACT, Cc><<<grid, 128, 0, st>>>(indptr, rowidx, v, lo, hi, g, r, (T)mu1, o)
     if (r <= 32)
@@ -287,6 +384,15 @@ static int csr_yt_chunked_dispatch(const int64_t *chunks, int64_t nchunks, const
     const T *v = (const T *)vals;
     const T *f = (const T *)FT;
     TY *o = (TY *)YT, *pp = (TY *)part;
+    if (sizeof(T) == 4 && v4_ok(r, FT)) {
+        csr_yt_chunk_v4_kernel<TY><<<grid, 128, 0, st>>>(chunks, nchunks, colidx,
+                                                         (const float *)vals, (const float *)FT, r,
+                                                         o, pp);
+        if (nheavy > 0)
+            csr_yt_fold_kernel<TY><<<(unsigned)((nheavy + 3) / 4), 128, 0, st>>>(heavy, nheavy, r,
+                                                                                 pp, o);
+        return launch_status();
+    }
 #define NMFB_CSRC(Cc) \
     csr_yt_chunk_kernel<T, TY, Cc><<<grid, 128, 0, st>>>(chunks, nchunks, colidx, v, f, r, o, pp)
     if (r <= 32)

@@ -1,0 +1,77 @@
+"""Sparse data products (the fast-path gathers) against fp64 numpy on
+Zipf-skewed CSC/CSR data: h = mu1 - G^T X (csc_linear) and Y^T = X F^T
+(csr_yt_chunked, heavy rows split into chunks and folded).  r % 4 == 0 takes
+the 16-byte vector-load kernels, other r the scalar ones; both must agree
+with fp64 to fp32 accumulation accuracy."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _csc(n, m, density, seed):
+    rng = np.random.default_rng(seed)
+    # Zipf-popular rows, skewed column counts, a few very heavy rows / columns
+    counts = np.minimum(rng.zipf(1.3, size=m), 3 * n // 4)
+    counts = np.maximum(1, (counts * density * n * m / counts.sum()).astype(np.int64))
+    counts[:3] = n // 2
+    pop = 1.0 / np.arange(1, n + 1)
+    pop /= pop.sum()
+    indptr = np.zeros(m + 1, dtype=np.int64)
+    rows, vals = [], []
+    for j in range(m):
+        rr = np.sort(rng.choice(n, size=min(int(counts[j]), n), replace=False, p=pop))
+        rows.append(rr)
+        vals.append(rng.exponential(size=len(rr)))
+        indptr[j + 1] = indptr[j] + len(rr)
+    return indptr, np.concatenate(rows).astype(np.int32), np.concatenate(vals)
+
+
+@pytest.mark.parametrize("r", [4, 50, 100, 128])
+def test_sparse_products_match_fp64(r):
+    import scipy.sparse as sp
+
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    n, m = 3000, 1200
+    indptr, rows, vals = _csc(n, m, 0.01, r)
+    X = sp.csc_matrix((vals, rows, indptr), shape=(n, m))
+    rng = np.random.default_rng(r)
+    G = rng.uniform(size=(n, r)).astype(np.float32)
+    FT = rng.uniform(size=(m, r)).astype(np.float32)
+    mu1 = 0.25
+    # csc_linear: h[col] = mu1 - sum_row G[row] v
+    h = torch.zeros((m, r), dtype=torch.float32, device=dev)
+    keep = []  # device inputs must outlive the asynchronous kernels
+
+    def t(a):
+        x = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        keep.append(x)
+        return x
+
+    ip, rw, vv = t(indptr), t(rows), t(vals.astype(np.float32))
+    L.call("nmfb_csc_linear", L.F32, L.MODE_FAST, D.vp(ip), D.vp(rw), D.vp(vv), 0, m, D.vp(t(G)),
+           r, mu1, D.vp(h), D.stream_handle())
+    Xf = X.astype(np.float32).astype(np.float64)
+    want_h = mu1 - (Xf.T @ G.astype(np.float64))
+    got_h = h.double().cpu().numpy()
+    scale = np.abs(Xf.T) @ np.abs(G.astype(np.float64)) + 1.0
+    assert np.max(np.abs(got_h - want_h) / scale) < 2e-6
+    # csr_yt_chunked: Y^T[row] = sum_col FT[col] v, fp64 accumulation
+    Xr = X.tocsr()
+    Xr.sort_indices()
+    rowptr = Xr.indptr.astype(np.int64)
+    chunks, heavy, nslots = D.csr_chunk_plan(rowptr, chunk=64)
+    assert len(heavy) > 0  # the heavy-row fold is exercised
+    yt = torch.zeros((n, r), dtype=torch.float64, device=dev)
+    part = torch.zeros((max(nslots, 1), r), dtype=torch.float64, device=dev)
+    L.call("nmfb_csr_yt_chunked", L.F32, D.vp(t(chunks)), len(chunks), D.vp(t(heavy)), len(heavy),
+           D.vp(t(Xr.indices.astype(np.int32))), D.vp(t(Xr.data.astype(np.float32))), D.vp(t(FT)),
+           r, L.F64, D.vp(yt), D.vp(part), D.stream_handle())
+    want_y = Xf @ FT.astype(np.float64)
+    got_y = yt.cpu().numpy()
+    assert np.max(np.abs(got_y - want_y) / (want_y + 1e-30)) < 1e-12
