@@ -30,10 +30,11 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const T *__restrict__
         ++ti;
     }
     const int tj = ti + t;
+    const bool diag = (ti == tj);  // diagonal tile: one operand serves both sides
     const int64_t row0 = (int64_t)blockIdx.y * chunk;
     const int64_t row1 = min(rows, row0 + chunk);
-    __shared__ T Ai[GROWS][GT];
-    __shared__ T Aj[GROWS][GT];
+    __shared__ __align__(16) T Ai[GROWS][GT];
+    __shared__ __align__(16) T Aj[GROWS][GT];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     double acc[4][4];
 #pragma unroll
@@ -41,16 +42,33 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const T *__restrict__
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
 
+    // software pipeline: the next slab's global loads are in flight in
+    // registers while the current slab is multiplied from shared memory
+    constexpr int PER = GROWS * GT / 256;  // elements per thread per operand
+    T pa[PER], pb[PER];
+    auto fetch = [&](int64_t rb) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = threadIdx.x + q * 256;
+            const int rr = idx / GT, c = idx % GT;
+            const int64_t row = rb + rr;
+            const int ci = ti * GT + c, cj = tj * GT + c;
+            const bool okr = row < row1;
+            pa[q] = (okr && ci < r) ? A[row * lda + ci] : T(0);
+            if (!diag) pb[q] = (okr && cj < r) ? A[row * lda + cj] : T(0);
+        }
+    };
+    if (row0 < row1) fetch(row0);
     for (int64_t rb = row0; rb < row1; rb += GROWS) {
-        for (int idx = threadIdx.x; idx < GROWS * GT; idx += 256) {
-            int rr = idx / GT, c = idx % GT;
-            int64_t row = rb + rr;
-            int ci = ti * GT + c, cj = tj * GT + c;
-            bool okr = row < row1;
-            Ai[rr][c] = (okr && ci < r) ? A[row * lda + ci] : T(0);
-            Aj[rr][c] = (okr && cj < r) ? A[row * lda + cj] : T(0);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = threadIdx.x + q * 256;
+            Ai[idx / GT][idx % GT] = pa[q];
+            if (!diag) Aj[idx / GT][idx % GT] = pb[q];
         }
         __syncthreads();
+        if (rb + GROWS < row1) fetch(rb + GROWS);
+        const T(*Bj)[GT] = diag ? Ai : Aj;
         T s[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -62,7 +80,7 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const T *__restrict__
 #pragma unroll
             for (int u = 0; u < 4; ++u) a[u] = Ai[rr][ty * 4 + u];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) b[v] = Aj[rr][tx * 4 + v];
+            for (int v = 0; v < 4; ++v) b[v] = Bj[rr][tx * 4 + v];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
