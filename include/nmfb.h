@@ -134,6 +134,13 @@ int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_i
  * with a fixed (deterministic) summation order; out = full symmetric r x r
  * fp64.  workspace: nmfb_gram_workspace_bytes(rows, r) bytes of device mem. */
 size_t nmfb_gram_workspace_bytes(int64_t rows, int32_t r);
+/* Gram with the anti-lopsided rescale fused into its epilogue: out = A^T A
+ * (as nmfb_gram), then Qa / scale_a / act_idx / active / ra_dev exactly as
+ * nmfb_rescale(dtype, out, r, diag_add, ...) would write them -- one stream-
+ * ordered pass, the last reducing CTA runs the rescale. */
+int nmfb_gram_rescale(int dtype, const void *A, int64_t rows, int32_t r, int64_t lda, double *out,
+                      void *workspace, double diag_add, void *Qa, void *scale_a, int32_t *act_idx,
+                      uint8_t *active, int32_t *ra_dev, void *stream);
 int nmfb_gram(int dtype, const void *A, int64_t rows, int32_t r, int64_t lda, double *out,
               void *workspace, void *stream);
 

@@ -11,6 +11,9 @@ namespace nmfb {
 size_t gram_workspace_bytes(int64_t rows, int r);
 int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, double *out, void *ws,
                 cudaStream_t st);
+int gram_rescale_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, double *out,
+                        void *ws, double diag_add, void *Qa, void *scale_a, int32_t *act_idx,
+                        uint8_t *active, int32_t *ra_dev, cudaStream_t st);
 int rescale_launch(int dtype, const double *G, int r, double diag_add, void *Qa, void *scale_a,
                    int32_t *act_idx, uint8_t *active, int32_t *ra_dev, double *full_scale,
                    cudaStream_t st);
@@ -163,6 +166,13 @@ int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_i
 }
 
 size_t nmfb_gram_workspace_bytes(int64_t rows, int32_t r) { return gram_workspace_bytes(rows, r); }
+
+int nmfb_gram_rescale(int dtype, const void *A, int64_t rows, int32_t r, int64_t lda, double *out,
+                      void *workspace, double diag_add, void *Qa, void *scale_a, int32_t *act_idx,
+                      uint8_t *active, int32_t *ra_dev, void *stream) {
+    return check(gram_rescale_launch(dtype, A, rows, r, lda, out, workspace, diag_add, Qa, scale_a,
+                                     act_idx, active, ra_dev, (cudaStream_t)stream));
+}
 
 int nmfb_gram(int dtype, const void *A, int64_t rows, int32_t r, int64_t lda, double *out,
               void *workspace, void *stream) {

@@ -143,7 +143,7 @@ static int64_t gram_chunk(int64_t rows) {
 size_t gram_workspace_bytes(int64_t rows, int r) {
     int64_t chunk = gram_chunk(rows);
     int64_t nchunk = rows > 0 ? (rows + chunk - 1) / chunk : 1;
-    return (size_t)nchunk * r * r * sizeof(double);
+    return (size_t)nchunk * r * r * sizeof(double) + 64;  // + the fused-rescale ticket
 }
 
 int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, double *out,
@@ -171,12 +171,14 @@ int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, doub
 // Rescale (single CTA): bit-exact restatement of nqp.rescale_arrays on
 // H = G + diag_add * I, compacted to the active dims (parallel.py:87-91).
 // ---------------------------------------------------------------------------
+// Rescale body, run by one CTA: bit-exact restatement of nqp.rescale_arrays
+// on H = G + diag_add * I, compacted to the active dims (parallel.py:87-91).
+// smem: 2 r doubles + r ints.  G is read with L2 (cg) loads so a CTA that did
+// not write it still sees the values other CTAs published before a fence.
 template <typename T>
-__global__ void __launch_bounds__(1024) rescale_kernel(const double *__restrict__ G, int r,
-                                                       double diag_add, T *Qa, T *scale_a,
-                                                       int32_t *act_idx, uint8_t *active,
-                                                       int32_t *ra_dev, double *full_scale) {
-    extern __shared__ double sh[];
+__device__ void rescale_body(const double *__restrict__ G, int r, double diag_add, T *Qa,
+                             T *scale_a, int32_t *act_idx, uint8_t *active, int32_t *ra_dev,
+                             double *full_scale, double *sh) {
     double *diag = sh;                         // r
     double *sq = sh + r;                       // r: sqrt(diag)
     int *pos = (int *)(sh + 2 * r);            // r: compact position or -1
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(1024) rescale_kernel(const double *__restrict_
     const int tid = threadIdx.x;
     for (int i = tid; i < r; i += blockDim.x) {
         // H = Q_g + (2.0 * mu2) * np.eye(r): the identity term adds diag_add * 1.0
-        const double d = __dadd_rn(G[i * r + i], __dmul_rn(diag_add, 1.0));
+        const double d = __dadd_rn(__ldcg(G + i * r + i), __dmul_rn(diag_add, 1.0));
         diag[i] = d;
         sq[i] = __dsqrt_rn(d);
     }
@@ -225,10 +227,94 @@ __global__ void __launch_bounds__(1024) rescale_kernel(const double *__restrict_
             v = 1.0;
         } else {
             // off-diagonal of H = G + diag_add * eye: G_ij + 0.0
-            v = __ddiv_rn(__dadd_rn(G[i * r + j], 0.0), __dmul_rn(sq[i], sq[j]));
+            v = __ddiv_rn(__dadd_rn(__ldcg(G + i * r + j), 0.0), __dmul_rn(sq[i], sq[j]));
         }
         Qa[pi * ra + pj] = (T)v;
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) rescale_kernel(const double *__restrict__ G, int r,
+                                                       double diag_add, T *Qa, T *scale_a,
+                                                       int32_t *act_idx, uint8_t *active,
+                                                       int32_t *ra_dev, double *full_scale) {
+    extern __shared__ double sh[];
+    rescale_body<T>(G, r, diag_add, Qa, scale_a, act_idx, active, ra_dev, full_scale, sh);
+}
+
+// Gram reduce with the rescale fused into its epilogue: the CTA that finishes
+// last (ticket) runs the rescale on the completed Gram -- one launch and no
+// host round trip between the Gram and the rescaled Q (north star (2)).
+template <typename T>
+__global__ void __launch_bounds__(256) gram_reduce_rescale_kernel(
+    const double *__restrict__ part, int nchunk, int r, double *__restrict__ out,
+    unsigned *ticket, double diag_add, T *Qa, T *scale_a, int32_t *act_idx, uint8_t *active,
+    int32_t *ra_dev) {
+    extern __shared__ double sh[];
+    __shared__ double red[8][32];
+    __shared__ bool last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int idx = blockIdx.x * 32 + lane;
+    const int a = idx / r, b = idx % r;
+    const bool upper = idx < r * r && a <= b;
+    double s = 0.0;
+    if (upper)
+        for (int c = warp; c < nchunk; c += 8) s += part[(int64_t)c * r * r + idx];
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && upper) {
+        double t = red[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) t += red[w][lane];
+        out[a * r + b] = t;
+        out[b * r + a] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    rescale_body<T>(out, r, diag_add, Qa, scale_a, act_idx, active, ra_dev, nullptr, sh);
+    if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch
+}
+
+int gram_rescale_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, double *out,
+                        void *ws, double diag_add, void *Qa, void *scale_a, int32_t *act_idx,
+                        uint8_t *active, int32_t *ra_dev, cudaStream_t st) {
+    if (r <= 0 || rows < 0 || r > 4096) return NMFB_ERR_ARG;
+    int64_t chunk = gram_chunk(rows);
+    int64_t nchunk = rows > 0 ? (rows + chunk - 1) / chunk : 1;
+    double *part = (double *)ws;
+    unsigned *ticket = (unsigned *)((char *)ws + (size_t)nchunk * r * r * sizeof(double));
+    cudaMemsetAsync(ticket, 0, sizeof(unsigned), st);
+    int ntile = (r + GT - 1) / GT;
+    dim3 grid(ntile * (ntile + 1) / 2, (unsigned)nchunk);
+    if (rows == 0)
+        cudaMemsetAsync(part, 0, sizeof(double) * r * r, st);
+    else if (dtype == NMFB_F64)
+        gram_partial_kernel<double><<<grid, 256, 0, st>>>((const double *)A, rows, r, lda, chunk,
+                                                          part);
+    else
+        gram_partial_kernel<float><<<grid, 256, 0, st>>>((const float *)A, rows, r, lda, chunk,
+                                                         part);
+    const size_t smem = 2 * r * sizeof(double) + r * sizeof(int);
+    const unsigned nb = (unsigned)((r * r + 31) / 32);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(gram_reduce_rescale_kernel<double>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gram_reduce_rescale_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (dtype == NMFB_F64)
+        gram_reduce_rescale_kernel<double><<<nb, 256, smem, st>>>(
+            part, (int)nchunk, r, out, ticket, diag_add, (double *)Qa, (double *)scale_a, act_idx,
+            active, ra_dev);
+    else
+        gram_reduce_rescale_kernel<float><<<nb, 256, smem, st>>>(
+            part, (int)nchunk, r, out, ticket, diag_add, (float *)Qa, (float *)scale_a, act_idx,
+            active, ra_dev);
+    return launch_status();
 }
 
 int rescale_launch(int dtype, const double *G, int r, double diag_add, void *Qa, void *scale_a,

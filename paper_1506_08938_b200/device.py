@@ -305,6 +305,11 @@ class Alternation:
         L.call("nmfb_gram", self.code, vp(A), rows, self.r, self.r, vp(out), vp(self.gram_ws),
                self._st())
 
+    def gram_rescale(self, A, rows, out, diag_add, side):
+        L.call("nmfb_gram_rescale", self.code, vp(A), rows, self.r, self.r, vp(out),
+               vp(self.gram_ws), diag_add, vp(self.Qa[side]), vp(self.sa[side]),
+               vp(self.act[side]), vp(self.active[side]), vp(self.ra[side]), self._st())
+
     def rescale(self, H, diag_add, side):
         L.call("nmfb_rescale", self.code, vp(H), self.r, diag_add, vp(self.Qa[side]),
                vp(self.sa[side]), vp(self.act[side]), vp(self.active[side]), vp(self.ra[side]),
@@ -330,9 +335,11 @@ class Alternation:
         cfg, d, r = self.cfg, self.d, self.r
         n, m = self.n, self.m
         if not self.qg_valid:
-            self.gram(self.G, n, self.Qg)
+            # Gram of G with the anti-lopsided rescale fused into its epilogue
+            self.gram_rescale(self.G, n, self.Qg, 2.0 * cfg.mu2, 0)
+        else:
+            self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
         self.qg_valid = False
-        self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
         st = self.stats[k, 0]
         if d.kind == "dense":
             if self.use_tc:
@@ -364,7 +371,9 @@ class Alternation:
         if self.prec == "fp64" or self.mode == L.MODE_REFERENCE:
             L.call("nmfb_hp_ref", self.code, vp(self.FT), m, r, bp, W, vp(self.Hf), self._st())
         else:
-            self.gram(self.FT, m, self.Hf)
+            # H_f = F F^T, rescaled for the component step right away
+            self.gram_rescale(self.FT, m, self.Hf, 2.0 * cfg.beta2, 1)
+            self.hf_rescaled = True
         if d.kind == "dense":
             if self.use_tc:
                 Ft = self.Ft[k % 2]
@@ -398,7 +407,9 @@ class Alternation:
         """Component step (parallel.run_mstep): NNLS over the n rows with
         h = beta1 - Y^T."""
         cfg = self.cfg
-        self.rescale(self.Hf, 2.0 * cfg.beta2, 1)
+        if not getattr(self, "hf_rescaled", False):
+            self.rescale(self.Hf, 2.0 * cfg.beta2, 1)
+        self.hf_rescaled = False
         st = self.stats[k, 1]
         if self.d.kind == "dense" and self.mode == L.MODE_FAST:
             self.nnls(1, self.ybuf, L.F32, self.splits_m, self.r, self.n * self.r, cfg.beta1,

@@ -106,3 +106,47 @@ def test_dropin_shard_kernels_fp64_bit_exact(kind, lo, hi):
     got = kernels.mstep_rows(YT1, 3, n, *margs, G2)
     assert got == want
     assert np.array_equal(G2, G1)
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("diag_add", [0.0, 0.02])
+@pytest.mark.parametrize("rows,r", [(1000, 10), (5000, 50), (3000, 100), (257, 130), (0, 8)])
+def test_gram_rescale_fused_equals_separate(dtype, diag_add, rows, r):
+    """nmfb_gram_rescale (rescale in the Gram reduce's epilogue) writes exactly
+    what nmfb_gram followed by nmfb_rescale writes -- including frozen dims."""
+    import torch
+
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    code = L.F64 if dtype == "fp64" else L.F32
+    tdt = torch.float64 if dtype == "fp64" else torch.float32
+    rng = np.random.default_rng(rows + r)
+    A = rng.exponential(size=(rows, r))
+    if r > 4:
+        A[:, 3] = 0.0  # a frozen (zero-diagonal) dimension
+    a = torch.from_numpy(A).to(dev, tdt)
+    ws = torch.zeros((L.lib().nmfb_gram_workspace_bytes(max(rows, 1), r) // 8 + 1,),
+                     dtype=torch.float64, device=dev)
+    outs = []
+    for fused in (True, False):
+        g = torch.zeros((r, r), dtype=torch.float64, device=dev)
+        Qa = torch.zeros((r * r,), dtype=tdt, device=dev)
+        sa = torch.zeros((r,), dtype=tdt, device=dev)
+        act = torch.zeros((r,), dtype=torch.int32, device=dev)
+        active = torch.zeros((r,), dtype=torch.uint8, device=dev)
+        ra = torch.zeros((1,), dtype=torch.int32, device=dev)
+        if fused:
+            L.call("nmfb_gram_rescale", code, D.vp(a), rows, r, r, D.vp(g), D.vp(ws), diag_add,
+                   D.vp(Qa), D.vp(sa), D.vp(act), D.vp(active), D.vp(ra), D.stream_handle())
+        else:
+            L.call("nmfb_gram", code, D.vp(a), rows, r, r, D.vp(g), D.vp(ws), D.stream_handle())
+            L.call("nmfb_rescale", code, D.vp(g), r, diag_add, D.vp(Qa), D.vp(sa), D.vp(act),
+                   D.vp(active), D.vp(ra), None, D.stream_handle())
+        torch.cuda.synchronize()
+        outs.append([x.cpu().numpy() for x in (g, Qa, sa, act, active, ra)])
+    for u, v in zip(*outs):
+        assert np.array_equal(u, v)
+    if r > 4 and rows > 0 and diag_add == 0.0:
+        assert outs[0][4][3] == 0 and int(outs[0][5][0]) == r - 1
