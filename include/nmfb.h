@@ -257,6 +257,11 @@ int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void 
 /* out[0] = sum a_i * b_i, out[1] = sum |a_i|, out[2] = sum a_i^2 (fp64,
  * deterministic).  b may be NULL (then out[0] = 0).  a_dtype / b_dtype. */
 size_t nmfb_dot_workspace_bytes(int64_t len);
+/* Data-matrix check in one pass: out[0] = number of entries that are negative
+ * or not finite, out[1] = sum |a|, out[2] = sum a^2 (fp64, deterministic);
+ * workspace: nmfb_dot_workspace_bytes. */
+int nmfb_data_stats(const void *a, int a_dtype, int64_t len, double *out, void *workspace,
+                    void *stream);
 int nmfb_dot(const void *a, int a_dtype, const void *b, int b_dtype, int64_t len, double *out,
              void *workspace, void *stream);
 

@@ -73,6 +73,7 @@ SIGNATURES = {
     "nmfb_dense_residual": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
     "nmfb_dense_residual_kmajor": (_int, [_vp, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
     "nmfb_dot_workspace_bytes": (_sz, [_i64]),
+    "nmfb_data_stats": (_int, [_vp, _int, _i64, _vp, _vp, _vp]),
     "nmfb_sum_parts": (_int, [_vp, _i32, _i64, _vp, _vp]),
     "nmfb_tc_gemm": (_int, [_vp, _i64, _i64, _vp, _vp, _i32, _vp, _i32, _i32, _vp]),
     "nmfb_tc_splits": (_int, [_i64, _i32]),
@@ -130,7 +131,7 @@ KERNELS_PER_CALL = {
     "nmfb_gemm_tall": 1, "nmfb_dense_linear_ref": 1, "nmfb_dense_yt_ref": 1, "nmfb_hp_ref": 1,
     "nmfb_csc_linear": 1, "nmfb_csr_yt": 1, "nmfb_dense_residual": 2, "nmfb_dot": 2,
     "nmfb_sum_parts": 1, "nmfb_dense_residual_kmajor": 2, "nmfb_csr_yt_chunked": 2, "nmfb_tc_gemm": 1, "nmfb_split_transpose": 1, "nmfb_transpose": 1,
-    "nmfb_slice_u8": 1, "nmfb_residual_i8": 2, "nmfb_gram_rescale": 2,
+    "nmfb_slice_u8": 1, "nmfb_residual_i8": 2, "nmfb_gram_rescale": 2, "nmfb_data_stats": 2,
 }
 
 

@@ -54,6 +54,8 @@ size_t residual_i8_workspace_bytes();
 int residual_i8_launch(const float *X, int64_t n, int64_t m, const void *Gsl, const void *Fsl,
                        int r, double *out, void *ws, cudaStream_t st);
 int tc_parts(int64_t M, int64_t K, int N, int splits);
+int data_stats_launch(const void *a, int a_dtype, int64_t len, double *out, void *ws,
+                      cudaStream_t st);
 int split_transpose_launch(const float *B, int64_t K, int r, float *hi, float *lo,
                            cudaStream_t st);
 int transpose_launch(const float *in, int64_t rows, int64_t cols, float *out, cudaStream_t st);
@@ -260,6 +262,11 @@ int nmfb_residual_i8(const float *X, int64_t n, int64_t m, const void *Gsl, cons
 }
 
 size_t nmfb_dot_workspace_bytes(int64_t len) { return dot_workspace_bytes(len); }
+
+int nmfb_data_stats(const void *a, int a_dtype, int64_t len, double *out, void *workspace,
+                    void *stream) {
+    return check(data_stats_launch(a, a_dtype, len, out, workspace, (cudaStream_t)stream));
+}
 
 int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void *stream) {
     return check(sum_parts_launch(parts, S, len, out, (cudaStream_t)stream));

@@ -9,7 +9,8 @@ namespace nmfb {
 
 constexpr int DOT_BLOCKS = 592;  // 4 x 148 SMs, fixed for determinism
 
-template <typename TA, typename TB>
+// BAD: slot 0 counts entries that are negative or not finite (data check)
+template <typename TA, typename TB, bool BAD = false>
 __global__ void __launch_bounds__(256) dot3_kernel(const TA *__restrict__ a,
                                                    const TB *__restrict__ b, int64_t len,
                                                    double *__restrict__ part) {
@@ -18,7 +19,10 @@ __global__ void __launch_bounds__(256) dot3_kernel(const TA *__restrict__ a,
     for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < len;
          i += (int64_t)gridDim.x * 256) {
         double x = (double)a[i];
-        if (b) s0 += x * (double)b[i];
+        if (BAD)
+            s0 += (x < 0.0 || !isfinite(x)) ? 1.0 : 0.0;
+        else if (b)
+            s0 += x * (double)b[i];
         s1 += fabs(x);
         s2 += x * x;
     }
@@ -72,6 +76,21 @@ int dot_launch(const void *a, int a_dtype, const void *b, int b_dtype, int64_t l
         dot_launch_a<double>((const double *)a, b, b_dtype, len, part, st);
     else
         dot_launch_a<float>((const float *)a, b, b_dtype, len, part, st);
+    dot3_final_kernel<<<1, 256, 0, st>>>(part, DOT_BLOCKS, out);
+    return launch_status();
+}
+
+// One pass over the data matrix: out = {#negative-or-nonfinite, sum|x|, sum x^2}
+// (require_nonnegative, matrix.py:169-178, and the init scale's mean).
+int data_stats_launch(const void *a, int a_dtype, int64_t len, double *out, void *ws,
+                      cudaStream_t st) {
+    double *part = (double *)ws;
+    if (a_dtype == NMFB_F64)
+        dot3_kernel<double, double, true><<<DOT_BLOCKS, 256, 0, st>>>((const double *)a, nullptr,
+                                                                      len, part);
+    else
+        dot3_kernel<float, float, true><<<DOT_BLOCKS, 256, 0, st>>>((const float *)a, nullptr,
+                                                                    len, part);
     dot3_final_kernel<<<1, 256, 0, st>>>(part, DOT_BLOCKS, out);
     return launch_status();
 }

@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(TC3_THREADS, 1)
             const int nch = (nkb + chunk_kb - 1) / chunk_kb;
             for (int c = 0; c < nch; ++c, ++g) {
                 const int buf = g & 1;
-                mbar_wait(&tmem_full[buf], (uint32_t)(g >> 1) & 1u);
+                mbar_wait_sleep(&tmem_full[buf], (uint32_t)(g >> 1) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t base = tmem + lane_base + (uint32_t)(buf * TC3_BM + half * 128);
 #pragma unroll

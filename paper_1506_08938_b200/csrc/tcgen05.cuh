@@ -34,6 +34,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Same, but the waiting thread may be suspended (woken when the phase
+// completes or after ~hint ns) instead of spinning: for warps that wait long
+// (epilogue / fold warps) so they do not steal issue slots from the warps
+// doing the work on the same scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra.uni WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(20000)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst,
                                             int c0, int c1) {
     asm volatile(

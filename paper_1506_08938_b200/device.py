@@ -219,8 +219,13 @@ class Alternation:
         n, m, r = data.n, data.m, cfg.rank
         self.n, self.m, self.r = n, m, r
         f64 = torch.float64
-        self.G = torch.as_tensor(np.ascontiguousarray(G0), dtype=dt).to(dev)
-        self.FT = torch.as_tensor(np.ascontiguousarray(FT0), dtype=dt).to(dev)
+        def _factor(A):
+            if isinstance(A, torch.Tensor):  # already on the device (torch-input fit)
+                return A.to(dev, dt).contiguous()
+            return torch.as_tensor(np.ascontiguousarray(A), dtype=dt).to(dev)
+
+        self.G = _factor(G0)
+        self.FT = _factor(FT0)
         self.Qg = torch.zeros((r, r), dtype=f64, device=dev)
         self.Hf = torch.zeros((r, r), dtype=f64, device=dev)
         # compact rescaled problems of the two steps
@@ -629,13 +634,14 @@ def validate_and_sum(data):
     from .exceptions import DataDomainError
 
     X = data.XT
-    if not bool(torch.isfinite(X).all()):
-        raise DataDomainError("data matrix contains NaN or Inf")
-    if X.numel() and float(X.min()) < 0:
-        raise DataDomainError("data matrix contains negative entries")
     ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=torch.float64,
                      device=X.device)
     out = torch.zeros((3,), dtype=torch.float64, device=X.device)
-    L.call("nmfb_dot", vp(X), _CODE[data.precision], None, L.F64, X.numel(), vp(out), vp(ws),
+    L.call("nmfb_data_stats", vp(X), _CODE[data.precision], X.numel(), vp(out), vp(ws),
            stream_handle())
-    return float(out[1].item())  # sum |x| == sum x for nonnegative data
+    bad, total, _ = out.tolist()
+    if bad > 0:
+        if not bool(torch.isfinite(X).all()):
+            raise DataDomainError("data matrix contains NaN or Inf")
+        raise DataDomainError("data matrix contains negative entries")
+    return float(total)  # sum |x| == sum x for nonnegative data

@@ -120,13 +120,32 @@ def initial_factors(V, cfg):
     return initial_factors_from_mean(n, m, _mean(V), cfg)
 
 
-def initial_factors_from_mean(n, m, mean, cfg):
+def initial_draws(n, m, cfg):
+    """The seeded U[0,1) draws of nmf.py:115-127 (G before F)."""
     rng = np.random.default_rng(cfg.seed)
+    return rng.uniform(size=(n, cfg.rank)), rng.uniform(size=(cfg.rank, m))
+
+
+def scale_draws(draws, mean, cfg):
+    u_g, u_f = draws
     scale = np.sqrt(mean / cfg.rank)
-    g = np.ascontiguousarray(rng.uniform(size=(n, cfg.rank)) * scale)
-    f = rng.uniform(size=(cfg.rank, m)) * scale
-    ft = np.ascontiguousarray(f.T)
+    g = np.ascontiguousarray(u_g * scale)
+    ft = np.ascontiguousarray((u_f * scale).T)
     return g, ft
+
+
+def scale_draws_device(draws, mean, cfg, device):
+    """scale_draws on the device (same fp64 products, so bit-identical factors;
+    the host only uploads the raw draws)."""
+    u_g, u_f = draws
+    scale = float(np.sqrt(mean / cfg.rank))
+    g = torch.from_numpy(u_g).to(device) * scale
+    ft = (torch.from_numpy(u_f).to(device) * scale).t().contiguous()
+    return g, ft
+
+
+def initial_factors_from_mean(n, m, mean, cfg):
+    return scale_draws(initial_draws(n, m, cfg), mean, cfg)
 
 
 def build_estep_problem(Q_g, V, col, G, cfg, warm=None):
@@ -189,11 +208,14 @@ class FitSession:
         if data is None and isinstance(V, torch.Tensor):
             # torch input (e.g. a pinned host buffer): upload first, validate
             # and take the mean for the init scale on the device
-            data = D.DeviceData(V, cfg.precision)
-            total = D.validate_and_sum(data)
+            data = D.DeviceData(V, cfg.precision)  # asynchronous upload
             n, m = data.n, data.m
+            # the init's uniform draws do not depend on the data: draw them on
+            # the host while the upload is in flight, scale once the mean is known
+            draws = initial_draws(n, m, cfg) if init is None else None
+            total = D.validate_and_sum(data)
             if init is None:
-                init = initial_factors_from_mean(n, m, total / (n * m), cfg)
+                init = scale_draws_device(draws, total / (n * m), cfg, data.device)
         elif data is None:
             V = _as_matrix(V)
             require_nonnegative(V, "data matrix")
