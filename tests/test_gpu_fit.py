@@ -276,3 +276,32 @@ def test_sparse_zipf_fp64_bit_exact_with_reference_gram():
     assert np.array_equal(st.G.cpu().numpy(), oG)
     assert np.array_equal(st.FT.cpu().numpy(), oFT)
     np.testing.assert_allclose(objs, olog.objective, rtol=1e-10)
+
+
+@pytest.mark.parametrize("n,m,r", [
+    (640, 960, 8),      # tcgen05 v3 GEMM, int8 residual (1 k-step)
+    (600, 1000, 50),    # v3 GEMM, int8 residual (2 k-steps)
+    (500, 700, 100),    # v2 GEMM (BN=112), int8 residual (KB=128, 4 k-steps)
+    (400, 560, 130),    # v2 GEMM (BN=144), FFMA residual (r > 128)
+    (333, 501, 20),     # m % 4 != 0: SIMT split-K GEMM + tile residual
+])
+def test_fp32_kernel_paths_teacher_forced(n, m, r):
+    """Every dense fp32 kernel path (chosen by r and alignment) reproduces the
+    oracle's outer iteration from the same state: objective to the north-star
+    1e-4 once past the decision-sensitive first iterations."""
+    from paper_1506_08938_b200 import NmfConfig
+
+    rng = np.random.default_rng(n + m + r)
+    W0 = rng.exponential(size=(n, r))
+    H0 = rng.exponential(size=(r, m))
+    x = W0 @ H0 + np.abs(rng.normal(0, 0.05, size=(n, m)))
+    ocfg = orc.Config(rank=r, seed=1, rel_change_tol=0.0, max_outer=1)
+    gcfg = NmfConfig(rank=r, seed=1, rel_change_tol=0.0, max_outer=1, precision="fp32")
+    res = _teacher_forced(x, ocfg, gcfg, ks=[0, 1, 2, 3, 4, 6, 8, 12, 16])
+    print(n, m, r, "teacher-forced rel:", " ".join(f"{k}:{rel:.1e}" for k, rel, *_ in res))
+    rels = np.array([rel for _, rel, *_ in res])
+    # the first iterations are decision-sensitive (eps = 0.1 approximate solves,
+    # as for config 1 above); once the factors settle every step is within 1e-4
+    assert rels.max() < 1e-3, rels
+    assert np.median(rels) < 1e-4, rels
+    assert (rels[-3:] < 1e-4).all(), rels
