@@ -37,18 +37,24 @@ BLOCK = L.FASTBREAK_BLOCK
 
 
 class ShardPlan:
-    """32-aligned column and row shards over `world` ranks (parallel.py:162-169)."""
+    """Column shards: 32-aligned near-equal blocks over `world` ranks
+    (parallel.py:162-169).  Row shards for the component step: uniform
+    32-aligned chunks (rank g owns rows [g c, min(n, (g+1) c)), c =
+    ceil(n / world / 32) * 32), so the row-blocked buffers are simply the
+    natural (n, r) layout padded to world * c rows: the reduce-scatter of Y^T
+    and the allgather of G need no repacking (the allgather runs in place)."""
 
     def __init__(self, n, m, world):
         self.n, self.m, self.world = n, m, world
         self.cols = D.block_plan(m, world)
-        self.rows = D.block_plan(n, world)
         while len(self.cols) < world:
             self.cols.append((m, m))
-        while len(self.rows) < world:
-            self.rows.append((n, n))
-        # reduce-scatter needs equal chunks: pad every row block to the largest
-        self.row_chunk = max(hi - lo for lo, hi in self.rows)
+        self.row_chunk = max(BLOCK, -(-n // world // BLOCK) * BLOCK) if n else BLOCK
+        while self.row_chunk * world < n:
+            self.row_chunk += BLOCK
+        self.rows = [(min(n, g * self.row_chunk), min(n, (g + 1) * self.row_chunk))
+                     for g in range(world)]
+        self.padded_rows = self.row_chunk * world
 
     def col_range(self, rank):
         return self.cols[rank]
@@ -79,35 +85,31 @@ class DistAlternation:
         return t
 
     def _reduce_scatter_rows(self, yt_full):
-        """yt_full (n, r) partial -> this rank's rows (row_chunk, r) summed."""
+        """Y^T partial -> this rank's rows summed over ranks.  yt_full is either
+        the padded (world * chunk, r) buffer (CUDA engine: no repacking) or the
+        natural (n, r) array (padded here)."""
         p = self.plan
-        r = yt_full.shape[1]
         chunk = p.row_chunk
-        if not self.comm:
-            lo, hi = p.row_range(0)
-            return yt_full[lo:hi]
-        padded = yt_full.new_zeros((self.world * chunk, r))
-        for g in range(self.world):
-            lo, hi = p.row_range(g)
-            padded[g * chunk: g * chunk + (hi - lo)] = yt_full[lo:hi]
-        out = yt_full.new_empty((chunk, r))
-        dist.reduce_scatter_tensor(out, padded, group=self.group)
         lo, hi = p.row_range(self.rank)
-        return out[: hi - lo]
-
-    def _allgather_rows(self, g_rows):
-        """this rank's G rows -> full G (n, r) on every rank."""
-        p = self.plan
         if not self.comm:
-            return g_rows
-        chunk = p.row_chunk
-        r = g_rows.shape[1]
-        send = g_rows.new_zeros((chunk, r))
-        send[: g_rows.shape[0]] = g_rows
-        recv = g_rows.new_empty((self.world * chunk, r))
-        dist.all_gather_into_tensor(recv, send, group=self.group)
-        parts = [recv[g * chunk: g * chunk + (hi - lo)] for g, (lo, hi) in enumerate(p.rows)]
-        return torch.cat(parts, 0)
+            return yt_full[lo:hi]
+        if yt_full.shape[0] != p.padded_rows:
+            padded = yt_full.new_zeros((p.padded_rows, yt_full.shape[1]))
+            padded[: p.n] = yt_full
+            yt_full = padded
+        if getattr(self, "_rs_out", None) is None or self._rs_out.dtype != yt_full.dtype:
+            self._rs_out = yt_full.new_empty((chunk, yt_full.shape[1]))
+        dist.reduce_scatter_tensor(self._rs_out, yt_full, group=self.group)
+        return self._rs_out[: hi - lo]
+
+    def _allgather_rows(self, g_pad):
+        """In place on the padded (world * chunk, r) G: my block -> everyone."""
+        p = self.plan
+        if self.comm:
+            chunk = p.row_chunk
+            mine = g_pad[self.rank * chunk: (self.rank + 1) * chunk]
+            dist.all_gather_into_tensor(g_pad, mine, group=self.group)
+        return g_pad
 
     # -- one outer iteration --------------------------------------------------
     def iterate(self, k):
@@ -122,10 +124,9 @@ class DistAlternation:
         Hf_part, yt_part = e.estep(k, clo)
         Hf = self._allreduce(Hf_part)
         yt_rows = self._reduce_scatter_rows(yt_part)
-        # component step on my rows
+        # component step on my rows, then every rank gets all of G
         e.mstep(k, Hf, yt_rows, rlo, rhi)
-        G_full = self._allgather_rows(e.g_rows(rlo, rhi))
-        e.set_g(G_full)
+        e.set_g(self._allgather_rows(e.g_padded(self.plan)))
         # objective pieces (sum over ranks)
         pieces = self._allreduce(e.objective_pieces(k, yt_rows, rlo, rhi))
         e.store_pieces(k, pieces)
@@ -151,6 +152,10 @@ class CudaEngine:
         # reduce-scatter; sparse / fp64: Y^T is already one fp64 buffer
         self.ysplit = self.data.kind == "dense" and st.mode == L.MODE_FAST
         ydt = torch.float32 if self.ysplit else st.ybuf.dtype
+        # row-blocked (padded) buffers: G and the Y^T partial live in the
+        # (world * chunk, r) layout of the collectives; st.G views the first n rows
+        self.g_pad = None
+        self.yt_pad = None
         self.yt = torch.zeros((self.data.n, self.r), dtype=ydt, device=dev)
         self.ycode = L.F32 if ydt == torch.float32 else L.F64
         self.n_total_cols = n_total_cols
@@ -169,18 +174,29 @@ class CudaEngine:
         self.st.Qg.copy_(Q)
         self.st.qg_valid = True
 
+    def bind_plan(self, plan):
+        """Allocate the padded row-blocked buffers of `plan` and move G into one."""
+        st, n, r = self.st, self.data.n, self.r
+        self.g_pad = torch.zeros((plan.padded_rows, r), dtype=st.G.dtype, device=st.G.device)
+        self.g_pad[:n].copy_(st.G)
+        st.G = self.g_pad[:n]
+        self.yt_pad = torch.zeros((plan.padded_rows, r), dtype=self.yt.dtype,
+                                  device=self.yt.device)
+        self.yt = self.yt_pad[:n]
+
     def estep(self, k, col_offset):
         st = self.st
         st.index_base_e = col_offset
         st.estep(k)
-        # partial accumulators of my columns: H_f partial, Y^T partial (summed split-K)
+        # partial accumulators of my columns: H_f partial, Y^T partial (summed
+        # split-K) written straight into the padded collective layout
         self.Hf_part.copy_(st.Hf)
         if self.ysplit:
             L.call("nmfb_sum_parts", D.vp(st.ybuf), st.splits_m, self.data.n * self.r,
                    D.vp(self.yt), D.stream_handle())
         else:
             self.yt.copy_(st.ybuf.view(self.data.n, self.r))
-        return self.Hf_part, self.yt
+        return self.Hf_part, (self.yt_pad if self.yt_pad is not None else self.yt)
 
     def mstep(self, k, Hf, yt_rows, lo, hi):
         st = self.st
@@ -194,11 +210,11 @@ class CudaEngine:
                    hi - lo, lo, float(self.cfg.epsilon), int(self.cfg.inner_cap), 0.0, None,
                    None, D.vp(stats), st.lanes, D.stream_handle())
 
-    def g_rows(self, lo, hi):
-        return self.st.G[lo:hi].contiguous()
+    def g_padded(self, plan):
+        return self.g_pad
 
     def set_g(self, G_full):
-        self.st.G.copy_(G_full)
+        pass  # the allgather filled st.G's padded buffer in place
 
     def objective_pieces(self, k, yt_rows, lo, hi):
         """Additive per-rank pieces (slot layout of device.Alternation):
@@ -256,6 +272,7 @@ class DistFit:
             raise ValueError("every rank must hold a 32-aligned equal column block")
         G0, FT0 = init
         self.engine = CudaEngine(X_block, cfg, G0, FT0, cfg.max_outer, m)
+        self.engine.bind_plan(self.plan)
         self.state = _StateView(DistAlternation(self.engine, self.plan, rank, group),
                                 self.engine.st)
 

@@ -62,11 +62,13 @@ class OracleEngine:
                                     self.cfg.epsilon, self.cfg.inner_cap, 0.0, self.G)
         assert fail == -1
 
-    def g_rows(self, lo, hi):
-        return torch.from_numpy(self.G[lo:hi].copy())
+    def g_padded(self, plan):
+        Gp = np.zeros((plan.padded_rows, self.r))
+        Gp[: self.G.shape[0]] = self.G
+        return torch.from_numpy(Gp)
 
     def set_g(self, G):
-        self.G = np.ascontiguousarray(G.numpy())
+        self.G = np.ascontiguousarray(G.numpy()[: self.G.shape[0]])
 
     def objective_pieces(self, k, yt_rows, lo, hi):
         clo, chi = self.cols
