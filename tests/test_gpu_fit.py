@@ -305,3 +305,20 @@ def test_fp32_kernel_paths_teacher_forced(n, m, r):
     assert rels.max() < 1e-3, rels
     assert np.median(rels) < 1e-4, rels
     assert (rels[-3:] < 1e-4).all(), rels
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -1.0])
+@pytest.mark.parametrize("as_torch", [False, True])
+def test_fit_rejects_bad_data(bad, as_torch):
+    """require_nonnegative (matrix.py:169-178): NaN / Inf / negative entries
+    raise DataDomainError before any factor update, numpy or torch input."""
+    import torch
+
+    from paper_1506_08938_b200 import NmfConfig, fit
+    from paper_1506_08938_b200.exceptions import DataDomainError
+
+    x = np.random.default_rng(0).uniform(size=(64, 96)).astype(np.float32)
+    x[5, 7] = bad
+    V = torch.from_numpy(x) if as_torch else x
+    with pytest.raises(DataDomainError):
+        fit(V, NmfConfig(rank=4, max_outer=2, precision="fp32"))
