@@ -211,6 +211,9 @@ def run_ours(args):
     hbm, peak_src = peaks()
     gname = "nmfb_tc_gemm" if "nmfb_tc_gemm" in calls else "nmfb_gemm_tall"
     gemm_calls, gemm_ms = calls.get(gname, (0, 0.0))
+    if "nmfb_tc_gemm_rows" in calls:  # multi-GPU peer path: X F^T stores into the owners
+        c2, t2 = calls["nmfb_tc_gemm_rows"]
+        gemm_calls, gemm_ms = gemm_calls + c2, gemm_ms + t2
     # algorithmic bytes per data-product launch, averaged over the two passes
     # (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once, B^T hi+lo, split-K C
     se, sm = getattr(st, "splits_e", 1), getattr(st, "splits_m", 1)
@@ -247,7 +250,10 @@ def run_ours(args):
                            "F F^T, X F^T, NNLS(n rows), objective",
                    "l2": "inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
                          % (n * m * 4 / 1e6),
-                   "parallelism": f"dp{world} (column-sharded)"},
+                   "parallelism": f"dp{world} (column-sharded)",
+                   "exchange": ("nvlink peer stores from the producing kernels"
+                                if getattr(sess, "peer", False) else
+                                ("nccl" if use_dist else "none"))},
         "roofline": {"kernel": gname + " (G^T X and X F^T passes over X; tcgen05 3xTF32)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_source": peak_src,

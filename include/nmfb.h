@@ -57,6 +57,9 @@ extern "C" {
 #define NMFB_MODE_FAST 0
 #define NMFB_MODE_REFERENCE 1
 
+/* largest world size of the peer-memory (NVLink) exchange entry points */
+#define NMFB_MAX_PEERS 8
+
 #define NMFB_FAIL_NONE (-1)      /* kernels.py:27 */
 #define NMFB_FASTBREAK_BLOCK 32  /* kernels.py:35 */
 #define NMFB_MAX_WORKERS 64
@@ -253,6 +256,51 @@ int nmfb_residual_i8(const float *X, int64_t n, int64_t m, const void *Gsl, cons
 /* out[i] = sum_{s < S} parts[s * len + i], fixed order (split-K partials of
  * X F^T summed before the multi-GPU reduce-scatter).  float32. */
 int nmfb_sum_parts(const float *parts, int32_t S, int64_t len, float *out, void *stream);
+
+/* ---- multi-GPU exchange over NVLink peer memory -----------------
+ * Replaces, for the column-sharded fit, the reference's process-level
+ * ordered reduce of the worker accumulators (parallel.reduce,
+ * parallel.py:141-159) and the shard fan-out of run_estep / run_mstep
+ * (parallel.py:94-133, 189-223): the data-product partials and solved rows
+ * move by peer stores issued from inside the producing kernels.  dst / flags
+ * / mirror are host arrays of `world` device pointers (peer mappings of
+ * symmetric buffers, e.g. torch symmetric memory); world <= NMFB_MAX_PEERS.
+ *
+ * nmfb_tc_gemm_rows: nmfb_tc_gemm whose partial slot s of row i is stored at
+ *   dst[o] + ((src * P + s) * chunk + i - o * chunk) * N, o = i / chunk,
+ *   P = nmfb_tc_parts(M, K, N, splits): owner o's receive buffer holds
+ *   world * P slots of (chunk x N) -- sum them in order (nmfb_nnls_batch with
+ *   h_parts = world * P, h_pstride = chunk * N).  world = 1, chunk = M is
+ *   nmfb_tc_gemm.  Requires chunk * world >= M.
+ * nmfb_nnls_batch_peers: nmfb_nnls_batch (fast mode) that also stores every
+ *   solution row j at mirror[q] + j * r (q < nmirror): the all-gather of the
+ *   solved rows fused into the solve.
+ * nmfb_peer_put: copy `bytes` (8-byte multiple) from src to dst[q] for every
+ *   q < world (src NULL: no copy); if signal, then store epoch into
+ *   flags[q][rank] for every q (release, system scope) once all of it is done.
+ *   ticket: a zero-initialised device word private to this rank.
+ * nmfb_peer_wait: wait until flags[q] >= epoch for all q < world (acquire,
+ *   system scope); after timeout_s the wait gives up and records epoch in
+ *   flags[world] (the caller checks it) instead of hanging the device.
+ * nmfb_sum_slots_f64: out[i] = sum_{s<S} slots[s * stride + i] in order. */
+int nmfb_tc_gemm_rows(const float *A, int64_t M, int64_t K, const float *Bt_hi,
+                      const float *Bt_lo, int32_t N, int32_t splits, float *const *dst,
+                      int32_t world, int64_t chunk, int32_t src, void *stream);
+int nmfb_nnls_batch_peers(int dtype, int mode, const void *Qa, const void *scale_a,
+                          const int32_t *act_idx, const uint8_t *active, int32_t r, int32_t ra,
+                          const int32_t *ra_dev, const void *h, int h_dtype, int32_t h_parts,
+                          int64_t h_ld, int64_t h_pstride, double h_base, void *x,
+                          int64_t count, int64_t index_base, double eps, int32_t max_inner,
+                          double max_stop0, int32_t *iters_out, void *final_out,
+                          uint64_t *stats, int32_t lanes, void *const *mirror, int32_t nmirror,
+                          void *stream);
+int nmfb_peer_put(const void *src, int64_t bytes, void *const *dst, int32_t world, int32_t rank,
+                  void *const *flags, uint32_t *ticket, uint64_t epoch, int32_t signal,
+                  void *stream);
+int nmfb_peer_wait(uint64_t *flags, int32_t world, uint64_t epoch, double timeout_s,
+                   void *stream);
+int nmfb_sum_slots_f64(const double *slots, int32_t S, int64_t len, int64_t stride,
+                       double *out, void *stream);
 
 /* out[0] = sum a_i * b_i, out[1] = sum |a_i|, out[2] = sum a_i^2 (fp64,
  * deterministic).  b may be NULL (then out[0] = 0).  a_dtype / b_dtype. */

@@ -15,7 +15,8 @@ import numpy as np
 from .exceptions import NumericalFailureError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libnmfb.so")
+# NMFB_LIB_PATH: an alternative in-tree build (A/B timing of two builds)
+LIB_PATH = os.environ.get("NMFB_LIB_PATH") or os.path.join(PKG, "libnmfb.so")
 
 NMFB_OK = 0
 NMFB_ERR_NUMERIC = 1
@@ -85,7 +86,22 @@ SIGNATURES = {
     "nmfb_split_transpose": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "nmfb_transpose": (_int, [_vp, _i64, _i64, _vp, _vp]),
     "nmfb_dot": (_int, [_vp, _int, _vp, _int, _i64, _vp, _vp, _vp]),
+    "nmfb_tc_gemm_rows": (_int, [_vp, _i64, _i64, _vp, _vp, _i32, _i32, _vp, _i32, _i64, _i32,
+                                 _vp]),
+    "nmfb_nnls_batch_peers": (_int, [_int, _int, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _int,
+                                     _i32, _i64, _i64, _f64, _vp, _i64, _i64, _f64, _i32, _f64,
+                                     _vp, _vp, _vp, _i32, _vp, _i32, _vp]),
+    "nmfb_peer_put": (_int, [_vp, _i64, _vp, _i32, _i32, _vp, _vp, ctypes.c_uint64, _i32, _vp]),
+    "nmfb_peer_wait": (_int, [_vp, _i32, ctypes.c_uint64, _f64, _vp]),
+    "nmfb_sum_slots_f64": (_int, [_vp, _i32, _i64, _i64, _vp, _vp]),
 }
+
+MAX_PEERS = 8  # NMFB_MAX_PEERS
+
+
+def ptr_array(ptrs):
+    """Host array of device pointers (the `void *const *` arguments)."""
+    return (ctypes.c_void_p * max(len(ptrs), 1))(*[ctypes.c_void_p(int(p)) for p in ptrs])
 
 _lib = None
 
@@ -103,6 +119,8 @@ def lib():
                 "(this package has no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("NMFB_LIB_PATH") and not hasattr(L, name):
+                continue  # an older A/B build may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
@@ -132,6 +150,8 @@ KERNELS_PER_CALL = {
     "nmfb_csc_linear": 1, "nmfb_csr_yt": 1, "nmfb_dense_residual": 2, "nmfb_dot": 2,
     "nmfb_sum_parts": 1, "nmfb_dense_residual_kmajor": 2, "nmfb_csr_yt_chunked": 2, "nmfb_tc_gemm": 1, "nmfb_split_transpose": 1, "nmfb_transpose": 1,
     "nmfb_slice_u8": 1, "nmfb_residual_i8": 2, "nmfb_gram_rescale": 2, "nmfb_data_stats": 2,
+    "nmfb_tc_gemm_rows": 1, "nmfb_nnls_batch_peers": 1, "nmfb_peer_put": 1, "nmfb_peer_wait": 1,
+    "nmfb_sum_slots_f64": 1,
 }
 
 

@@ -48,6 +48,16 @@ int dense_residual_kmajor_launch(const float *XT, int64_t m, int64_t n, const fl
 int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
                    int N, float *C, int splits, int stages, cudaStream_t st);
 int tc_effective_splits(int64_t K, int splits);
+int tc_gemm_rows_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi,
+                        const float *Bt_lo, int N, const RowOut &out, int splits, int stages,
+                        cudaStream_t st);
+int peer_put_launch(const void *src, int64_t bytes, void *const *dst, int world, int rank,
+                    void *const *flags, unsigned *ticket, unsigned long long epoch, int signal,
+                    cudaStream_t st);
+int peer_wait_launch(void *flags, int world, unsigned long long epoch, double timeout_s,
+                     cudaStream_t st);
+int sum_slots_f64_launch(const double *slots, int S, int64_t len, int64_t stride, double *out,
+                         cudaStream_t st);
 size_t slice_bytes(int64_t rows, int r);
 int slice_u8_launch(const float *A, int64_t rows, int r, int64_t lda, void *out, cudaStream_t st);
 size_t residual_i8_workspace_bytes();
@@ -125,6 +135,48 @@ int nmfb_nnls_batch(int dtype, int mode, const void *Qa, const void *scale_a,
     p.lanes = lanes;
     p.stream = (cudaStream_t)stream;
     if (h_parts < 0 || eps < 0.0 || eps > 1.0 || !stats) return NMFB_ERR_ARG;
+    return check(nnls_launch(p));
+}
+
+int nmfb_nnls_batch_peers(int dtype, int mode, const void *Qa, const void *scale_a,
+                          const int32_t *act_idx, const uint8_t *active, int32_t r, int32_t ra,
+                          const int32_t *ra_dev, const void *h, int h_dtype, int32_t h_parts,
+                          int64_t h_ld, int64_t h_pstride, double h_base, void *x,
+                          int64_t count, int64_t index_base, double eps, int32_t max_inner,
+                          double max_stop0, int32_t *iters_out, void *final_out,
+                          uint64_t *stats, int32_t lanes, void *const *mirror, int32_t nmirror,
+                          void *stream) {
+    NnlsLaunch p;
+    p.dtype = dtype;
+    p.mode = mode;
+    p.Qa = Qa;
+    p.scale_a = scale_a;
+    p.act_idx = act_idx;
+    p.active = active;
+    p.r = r;
+    p.ra = ra;
+    p.ra_dev = ra_dev;
+    p.h = h;
+    p.h_dtype = h_dtype;
+    p.h_parts = h_parts;
+    p.h_ld = h_ld;
+    p.h_pstride = h_pstride;
+    p.h_base = h_base;
+    p.x = x;
+    p.count = count;
+    p.index_base = index_base;
+    p.eps = eps;
+    p.max_inner = max_inner;
+    p.max_stop0 = max_stop0;
+    p.iters_out = iters_out;
+    p.final_out = final_out;
+    p.stats = (unsigned long long *)stats;
+    p.lanes = lanes;
+    p.stream = (cudaStream_t)stream;
+    if (h_parts < 0 || eps < 0.0 || eps > 1.0 || !stats) return NMFB_ERR_ARG;
+    if (nmirror < 0 || nmirror > NMFB_MAX_PEERS || (nmirror > 0 && !mirror)) return NMFB_ERR_ARG;
+    p.nmirror = nmirror;
+    for (int q = 0; q < nmirror; ++q) p.mirror[q] = mirror[q];
     return check(nnls_launch(p));
 }
 
@@ -276,6 +328,37 @@ int nmfb_tc_gemm(const float *A, int64_t M, int64_t K, const float *Bt_hi, const
                  int32_t N, float *C, int32_t splits, int32_t stages, void *stream) {
     return check(tc_gemm_launch(A, M, K, Bt_hi, Bt_lo, N, C, splits, stages,
                                 (cudaStream_t)stream));
+}
+
+int nmfb_tc_gemm_rows(const float *A, int64_t M, int64_t K, const float *Bt_hi,
+                      const float *Bt_lo, int32_t N, int32_t splits, float *const *dst,
+                      int32_t world, int64_t chunk, int32_t src, void *stream) {
+    if (!dst || world < 1 || world > NMFB_MAX_PEERS) return NMFB_ERR_ARG;
+    RowOut out{};
+    for (int q = 0; q < world; ++q) out.dst[q] = dst[q];
+    out.world = world;
+    out.src = src;
+    out.chunk = chunk;
+    return check(tc_gemm_rows_launch(A, M, K, Bt_hi, Bt_lo, N, out, splits, 0,
+                                     (cudaStream_t)stream));
+}
+
+int nmfb_peer_put(const void *src, int64_t bytes, void *const *dst, int32_t world, int32_t rank,
+                  void *const *flags, uint32_t *ticket, uint64_t epoch, int32_t signal,
+                  void *stream) {
+    return check(peer_put_launch(src, bytes, dst, world, rank, flags, ticket,
+                                 (unsigned long long)epoch, signal, (cudaStream_t)stream));
+}
+
+int nmfb_peer_wait(uint64_t *flags, int32_t world, uint64_t epoch, double timeout_s,
+                   void *stream) {
+    return check(peer_wait_launch(flags, world, (unsigned long long)epoch, timeout_s,
+                                  (cudaStream_t)stream));
+}
+
+int nmfb_sum_slots_f64(const double *slots, int32_t S, int64_t len, int64_t stride,
+                       double *out, void *stream) {
+    return check(sum_slots_f64_launch(slots, S, len, stride, out, (cudaStream_t)stream));
 }
 
 int nmfb_tc_splits(int64_t K, int32_t splits) { return tc_effective_splits(K, splits); }

@@ -34,6 +34,22 @@ struct NnlsLaunch {
     bool independent = false;
     int lanes;  // 0 = auto
     cudaStream_t stream;
+    // fused all-gather (multi-GPU): every solution row is also stored at the
+    // same offset from each mirror base (peer GPUs' copies of x, NVLink)
+    void *mirror[NMFB_MAX_PEERS] = {};
+    int nmirror = 0;
+};
+
+// Placement of a GEMM's partial slots.  Row i of slot s is written to
+//   dst[o] + ((src * parts + s) * chunk + (i - o * chunk)) * N,   o = i / chunk.
+// world = 1, chunk = M: the plain [slot][M][N] layout.  world > 1: each owner
+// o's 32-aligned row chunk lands directly in o's receive buffer (peer stores
+// over NVLink), so the epilogue IS the reduce-scatter's transfer and owner o
+// sums its world * parts slots in a fixed order.
+struct RowOut {
+    float *dst[NMFB_MAX_PEERS];
+    int world, src;
+    int64_t chunk;
 };
 
 int nnls_launch(const NnlsLaunch &p);

@@ -53,6 +53,12 @@ int nnls_launch(const NnlsLaunch &p) {
     if (p.count <= 0) return NMFB_OK;
     if (p.r <= 0 || p.ra < 0 || p.ra > p.r || p.index_base < 0 || p.max_inner < 1)
         return NMFB_ERR_ARG;
+    if (p.nmirror < 0 || p.nmirror > NMFB_MAX_PEERS) return NMFB_ERR_ARG;
+    for (int q = 0; q < p.nmirror; ++q)
+        if (!p.mirror[q]) return NMFB_ERR_ARG;
+    // the fused all-gather lives in the fast kernel only
+    if (p.nmirror > 0 && (p.dtype == NMFB_F64 || p.mode == NMFB_MODE_REFERENCE))
+        return NMFB_ERR_ARG;
     if (p.dtype == NMFB_F64) {
         if (p.h_dtype != NMFB_F64) return NMFB_ERR_ARG;
         return launch_ref_impl<double, double>(p);

@@ -30,6 +30,8 @@ struct NnlsArgs {
     int hist_ld;             // reference kernel only (nqp.solve histories)
     bool independent;        // every problem its own fast-break scope (nqp.solve)
     unsigned long long *stats;  // [0] += inner iterations, [1] = min failing global index
+    T *mirror[NMFB_MAX_PEERS];  // fast kernel: solution rows also stored here (peer GPUs)
+    int nmirror;
 };
 
 template <typename T, typename TH, typename O>
@@ -69,6 +71,8 @@ static NnlsArgs<T, TH> make_args(const NnlsLaunch &p) {
     a.hist_ld = p.hist_ld;
     a.independent = p.independent;
     a.stats = (unsigned long long *)p.stats;
+    a.nmirror = p.nmirror;
+    for (int q = 0; q < NMFB_MAX_PEERS; ++q) a.mirror[q] = q < p.nmirror ? (T *)p.mirror[q] : nullptr;
     return a;
 }
 

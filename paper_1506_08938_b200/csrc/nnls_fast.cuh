@@ -1,5 +1,7 @@
 // Fast fp32 batched NNLS (warp-group per problem); see nnls.cu.
 #pragma once
+#include <type_traits>
+
 #include "nnls_common.cuh"
 
 namespace nmfb {
@@ -85,7 +87,10 @@ __host__ __device__ constexpr int nnls_min_blocks(int E, int L, int threads) {
     return (65536 / (nnls_regs(E, L) * threads)) < 1 ? 1 : (65536 / (nnls_regs(E, L) * threads));
 }
 
-template <typename TH, int E, int L, int B>
+// MIRROR: the solution rows are also stored into a.mirror[] (fused
+// all-gather of the multi-GPU path) -- a separate instantiation, so the
+// single-GPU kernel carries no extra code
+template <typename TH, int E, int L, int B, bool MIRROR>
 __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     nnls_fast_kernel(NnlsArgs<float, TH> a) {
     constexpr int R = E * L;
@@ -367,6 +372,15 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                 if (k < ra) a.x[j * r + a.act_idx[k]] = __fdiv_rn(y[e], a.scale_a[k]);
             }
         }
+        if (MIRROR && (write_x || !any_neg)) {
+            // fused all-gather: the finished row (read back after the group's
+            // stores) goes to the same offset in every mirror (peer GPUs)
+            __syncwarp(gmask);
+            for (int i = l; i < r; i += L) {
+                const float v = a.x[j * r + i];
+                for (int q = 0; q < a.nmirror; ++q) a.mirror[q][j * r + i] = v;
+            }
+        }
         if (l == 0) {
             if (a.iters_out) a.iters_out[j] = fail ? -1 : iters;
             if (a.final_out) a.final_out[j] = fail ? 0.f : final_norm;
@@ -385,7 +399,13 @@ static int launch_fast_variant(const NnlsLaunch &p) {
     constexpr int R = E * L, S = R | 1;
     // Q (R x S) + one staged h row (r floats) per problem slot
     size_t smem = sizeof(float) * ((size_t)R * S + (size_t)32 * B * p.r);
-    auto kern = nnls_fast_kernel<TH, E, L, B>;
+    auto kern = nnls_fast_kernel<TH, E, L, B, false>;
+    if (p.nmirror > 0) {
+        if constexpr (std::is_same<TH, float>::value)
+            kern = nnls_fast_kernel<TH, E, L, B, true>;
+        else
+            return NMFB_ERR_ARG;  // the fused all-gather takes fp32 partials
+    }
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (launch_status() != NMFB_OK) return NMFB_ERR_CUDA;

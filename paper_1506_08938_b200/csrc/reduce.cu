@@ -95,36 +95,31 @@ int data_stats_launch(const void *a, int a_dtype, int64_t len, double *out, void
     return launch_status();
 }
 
-// out[i] = sum_{s < S} parts[s * len + i] in s order (split-K partials of a
-// data product summed before a collective; float32, float4-vectorised)
+// out[i] = sum_{s < S} parts[s * len + i] (split-K partials of a data
+// product summed before a collective; float32).  The summation order is the
+// NNLS prologue's (fast_h, nnls_fast.cuh: four interleaved accumulators), so a
+// world-1 collective path reproduces the single-GPU linear terms bit for bit.
 __global__ void sum_parts_f32_kernel(const float *__restrict__ parts, int S, int64_t len,
                                      float *__restrict__ out) {
-    int64_t i4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i4 >= len) return;
-    if (i4 + 3 < len && (len % 4) == 0) {
-        float4 acc = *reinterpret_cast<const float4 *>(parts + i4);
-        for (int s = 1; s < S; ++s) {
-            float4 v = *reinterpret_cast<const float4 *>(parts + (int64_t)s * len + i4);
-            acc.x += v.x;
-            acc.y += v.y;
-            acc.z += v.z;
-            acc.w += v.w;
-        }
-        *reinterpret_cast<float4 *>(out + i4) = acc;
-    } else {
-        for (int64_t i = i4; i < min(len, i4 + 4); ++i) {
-            float acc = parts[i];
-            for (int s = 1; s < S; ++s) acc += parts[(int64_t)s * len + i];
-            out[i] = acc;
-        }
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    const float *p = parts + i;
+    float s0 = p[0], s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int k = 1;
+    for (; k + 3 < S; k += 4) {
+        s0 += p[(int64_t)k * len];
+        s1 += p[(int64_t)(k + 1) * len];
+        s2 += p[(int64_t)(k + 2) * len];
+        s3 += p[(int64_t)(k + 3) * len];
     }
+    for (; k < S; ++k) s0 += p[(int64_t)k * len];
+    out[i] = (s0 + s1) + (s2 + s3);
 }
 
 int sum_parts_launch(const float *parts, int S, int64_t len, float *out, cudaStream_t st) {
     if (len <= 0) return NMFB_OK;
     if (S < 1) return NMFB_ERR_ARG;
-    int64_t threads = (len + 3) / 4;
-    sum_parts_f32_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(parts, S, len, out);
+    sum_parts_f32_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(parts, S, len, out);
     return launch_status();
 }
 

@@ -324,11 +324,56 @@ __device__ __forceinline__ void for_each_segment(const TcSched &s, int b, F &&f)
     }
 }
 
+// element offset of row i of partial slot `slot` inside its owner's buffer
+// (RowOut layout); *owner receives the destination rank
+__device__ __forceinline__ int64_t rowout_off(const RowOut &o, int parts, int slot, int i,
+                                              int N, int *owner) {
+    const int chunk = (int)o.chunk;  // rows fit in int (M is an int)
+    const int g = i / chunk;
+    *owner = g;
+    return ((int64_t)(o.src * parts + slot) * chunk + (i - g * chunk)) * N;
+}
+
+// Store one fold thread's column (factor column fcol of 128 consecutive rows
+// row0.., values v(q)) into partial slot `part`.  row0 is a multiple of 128
+// and a multi-GPU owner chunk a multiple of 32 (world = 1: one owner), so a
+// 32-row group never straddles two owners: the destination base is derived
+// once per group and the stores stay a plain strided sequence.
+template <class V>
+__device__ __forceinline__ void store_col128(const RowOut &out, int parts, int part, int row0,
+                                             int M, int N, int fcol, V v) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int rg = row0 + 32 * g;
+        if (rg < M) {
+            int o;
+            const int64_t off = rowout_off(out, parts, part, rg, N, &o) + fcol;
+            float *p = out.dst[o] + off;
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+                if (rg + q < M) p[(int64_t)q * N] = v(32 * g + q);
+        }
+    }
+}
+// Zero fill of an unused slot (rare: the tile's last segment): not unrolled
+__device__ __noinline__ void zero_col128(const RowOut &out, int parts, int part, int row0, int M,
+                                         int N, int fcol) {
+    for (int g = 0; g < 4; ++g) {
+        const int rg = row0 + 32 * g;
+        if (rg >= M) break;
+        int o;
+        const int64_t off = rowout_off(out, parts, part, rg, N, &o) + fcol;
+        float *p = out.dst[o] + off;
+        for (int q = 0; q < 32 && rg + q < M; ++q) p[(int64_t)q * N] = 0.f;
+    }
+}
+
+
 template <int BN>
 __global__ void __launch_bounds__(TC2_THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmBlo, float *__restrict__ C, int M, int N,
-                    const TcSched sched, int NS, int chunk_kb, int64_t slot_stride, int dbg) {
+                    const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ RowOut out,
+                    int M, int N, const TcSched sched, int NS, int chunk_kb, int dbg) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     constexpr uint32_t a_bytes = TC_BM * TC_BK * 4;
@@ -496,13 +541,15 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
             }
             const int row = tile * TC_BM + row_in_tile;
             if (row < M) {
-                float *crow = C + (int64_t)slot * slot_stride + (int64_t)row * N;
+                int o;
+                const int64_t off = rowout_off(out, sched.parts, slot, row, N, &o);
+                float *crow = out.dst[o] + off;
 #pragma unroll
                 for (int q = 0; q < BN; ++q)
                     if (q < N) crow[q] = run[q];
                 if (zero_tail) {
                     for (int s2 = slot + 1; s2 < sched.parts; ++s2) {
-                        float *z = C + (int64_t)s2 * slot_stride + (int64_t)row * N;
+                        float *z = out.dst[o] + rowout_off(out, sched.parts, s2, row, N, &o);
                         for (int q = 0; q < N; ++q) z[q] = 0.f;
                     }
                 }
@@ -605,8 +652,8 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 
 __global__ void __launch_bounds__(TC3_THREADS, 1)
     tc_gemm3_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmBlo, float *__restrict__ C, int M, int N,
-                    const TcSched sched, int chunk_kb, int64_t slot_stride, int dbg) {
+                    const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ RowOut out,
+                    int M, int N, const TcSched sched, int chunk_kb, int dbg) {
     // separate rings: X (HBM, ~2 us TMA latency under load -> deep), F' (L2,
     // shallow) and the split products [X_lo bf16 | F_hi bf16]
     constexpr int NX = TC3_NX, NF = TC3_NF, NL = TC3_NL;
@@ -822,16 +869,11 @@ __global__ void __launch_bounds__(TC3_THREADS, 1)
             if (fcol < N) {
                 const int part = 2 * slot + lohi;
                 const int row0 = tile * TC3_BM + half * 128;
-                float *cp = C + (int64_t)part * slot_stride + fcol;
-#pragma unroll
-                for (int q = 0; q < 128; ++q)
-                    if (row0 + q < M) cp[(int64_t)(row0 + q) * N] = run[q];
+                store_col128(out, sched.parts, part, row0, M, N, fcol,
+                             [&](int q) { return run[q]; });
                 if (zero_tail) {
-                    for (int p2 = part + 2; p2 < sched.parts; p2 += 2) {
-                        float *z = C + (int64_t)p2 * slot_stride + fcol;
-                        for (int q = 0; q < 128; ++q)
-                            if (row0 + q < M) z[(int64_t)(row0 + q) * N] = 0.f;
-                    }
+                    for (int p2 = part + 2; p2 < sched.parts; p2 += 2)
+                        zero_col128(out, sched.parts, p2, row0, M, N, fcol);
                 }
             }
         });
@@ -970,7 +1012,8 @@ int tc_parts(int64_t M, int64_t K, int N, int splits) {
 }
 
 static void launch_tc3(const CUtensorMap &tx, const CUtensorMap &tb, const CUtensorMap &tbl,
-                       float *C, int M, int N, const TcSched &s, int chunk_kb, cudaStream_t st) {
+                       const RowOut &out, int M, int N, const TcSched &s, int chunk_kb,
+                       cudaStream_t st) {
     static bool attr = false;
     const size_t smem = (size_t)TC3_NX * TC3_BM * TC_BK * 4 + (size_t)TC3_NF * 128 * TC_BK * 4 +
                         (size_t)TC3_NL * (TC3_BM + 128) * TC_BK * 2 + 256 + 1024;
@@ -980,14 +1023,13 @@ static void launch_tc3(const CUtensorMap &tx, const CUtensorMap &tb, const CUten
         attr = true;
     }
     static const int dbg = getenv("NMFB_TC_DEBUG") ? atoi(getenv("NMFB_TC_DEBUG")) : 0;
-    tc_gemm3_kernel<<<s.G, TC3_THREADS, smem, st>>>(tx, tb, tbl, C, M, N, s, chunk_kb,
-                                                    (int64_t)M * N, dbg);
+    tc_gemm3_kernel<<<s.G, TC3_THREADS, smem, st>>>(tx, tb, tbl, out, M, N, s, chunk_kb, dbg);
 }
 
 template <int BN>
 static void launch_tc2(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &tbl,
-                       float *C, int M, int N, const TcSched &s, int stages, int chunk_kb,
-                       cudaStream_t st) {
+                       const RowOut &out, int M, int N, const TcSched &s, int stages,
+                       int chunk_kb, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc_gemm2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1002,8 +1044,8 @@ static void launch_tc2(const CUtensorMap &ta, const CUtensorMap &tb, const CUten
     const size_t smem = std::max<size_t>(smem_of(ns), 116 * 1024);
     // NMFB_TC_DEBUG=1: TMA stream only, =2: TMA + A_lo split (no MMA) -- tuning aid
     static const int dbg = getenv("NMFB_TC_DEBUG") ? atoi(getenv("NMFB_TC_DEBUG")) : 0;
-    tc_gemm2_kernel<BN><<<s.G, TC2_THREADS, smem, st>>>(ta, tb, tbl, C, M, N, s, ns, chunk_kb,
-                                                        (int64_t)M * N, dbg);
+    tc_gemm2_kernel<BN><<<s.G, TC2_THREADS, smem, st>>>(ta, tb, tbl, out, M, N, s, ns, chunk_kb,
+                                                        dbg);
 }
 
 extern "C" int nmfb_debug_tc3_timeline(long long *host_out) {
@@ -1013,9 +1055,18 @@ extern "C" int nmfb_debug_tc3_cta(long long *host_out) {
     return cudaMemcpyFromSymbol(host_out, g_tc3_cta, sizeof(g_tc3_cta)) == cudaSuccess ? 0 : 3;
 }
 
-int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
-                   int N, float *C, int splits, int stages, cudaStream_t st) {
+int tc_gemm_rows_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi,
+                        const float *Bt_lo, int N, const RowOut &out, int splits, int stages,
+                        cudaStream_t st) {
     if (M <= 0 || K <= 0 || N <= 0 || N > 160) return NMFB_ERR_ARG;
+    if (out.world < 1 || out.world > NMFB_MAX_PEERS || out.src < 0 || out.src >= out.world ||
+        out.chunk <= 0 || out.chunk * out.world < M || out.chunk > INT32_MAX)
+        return NMFB_ERR_ARG;
+    // owner chunks are whole 32-row groups (fast-break blocks; the v3
+    // epilogue stores 32-row groups)
+    if (out.world > 1 && out.chunk % 32 != 0) return NMFB_ERR_ARG;
+    for (int o = 0; o < out.world; ++o)
+        if (!out.dst[o]) return NMFB_ERR_ARG;
     if ((K * 4) % 16 != 0) return NMFB_ERR_ARG;  // TMA row pitch must be 16-byte aligned
     if (((uintptr_t)A | (uintptr_t)Bt_hi | (uintptr_t)Bt_lo) % 16 != 0) return NMFB_ERR_ARG;
     const int BN = ((N + 15) / 16) * 16;
@@ -1035,7 +1086,7 @@ int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, con
     // into the round-to-nearest running sum; NMFB_TC_CHUNK overrides for tuning
     static const int chunk_env = getenv("NMFB_TC_CHUNK") ? atoi(getenv("NMFB_TC_CHUNK")) : 0;
     if (variant == TC_V3) {
-        launch_tc3(ta, tb, tbl, C, (int)M, N, s, chunk_env > 0 ? chunk_env : 4, st);
+        launch_tc3(ta, tb, tbl, out, (int)M, N, s, chunk_env > 0 ? chunk_env : 4, st);
         return launch_status();
     }
     if (variant == TC_V2) {
@@ -1043,7 +1094,7 @@ int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, con
         switch (BN) {
 #define NMFB_TC2_CASE(bn)                                                                  \
     case bn:                                                                               \
-        launch_tc2<bn>(ta, tb, tbl, C, (int)M, N, s, stages, chunk_kb, st);                \
+        launch_tc2<bn>(ta, tb, tbl, out, (int)M, N, s, stages, chunk_kb, st);              \
         break;
             NMFB_TC2_CASE(16) NMFB_TC2_CASE(32) NMFB_TC2_CASE(48) NMFB_TC2_CASE(64)
             NMFB_TC2_CASE(80) NMFB_TC2_CASE(96) NMFB_TC2_CASE(112) NMFB_TC2_CASE(128)
@@ -1054,7 +1105,9 @@ int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, con
         }
         return launch_status();
     }
-    // classic (non-persistent) kernel, kept for comparison
+    // classic (non-persistent) kernel, kept for comparison (plain layout only)
+    if (out.world != 1 || out.chunk != M) return NMFB_ERR_ARG;
+    float *C = out.dst[0];
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1070,6 +1123,16 @@ int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, con
                                                    s.kb_per_split, stages, chunk_kb,
                                                    (int64_t)M * N);
     return launch_status();
+}
+
+int tc_gemm_launch(const float *A, int64_t M, int64_t K, const float *Bt_hi, const float *Bt_lo,
+                   int N, float *C, int splits, int stages, cudaStream_t st) {
+    RowOut out{};
+    out.dst[0] = C;
+    out.world = 1;
+    out.src = 0;
+    out.chunk = M > 0 ? M : 1;
+    return tc_gemm_rows_launch(A, M, K, Bt_hi, Bt_lo, N, out, splits, stages, st);
 }
 
 int tc_effective_splits(int64_t K, int splits) {

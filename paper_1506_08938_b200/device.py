@@ -294,6 +294,9 @@ class Alternation:
         self.qg_valid = False
         self.index_base_e = 0  # global column of FT row 0 (multi-GPU column shards)
         self.gt_valid = False  # Gt holds tf32-split G^T of the current G
+        # multi-GPU peer layout of the X F^T partials (dist.PeerExchange):
+        # (dst pointer array, world, chunk, src rank) or None = local ybuf
+        self.yt_out = None
 
     @staticmethod
     def _splits(M, K, sms):
@@ -385,8 +388,14 @@ class Alternation:
                 self._wait_residual(k % 2)  # residual(k-2) still reads this parity
                 L.call("nmfb_split_transpose", vp(self.FT), m, r, vp(Ft[0]), vp(Ft[1]),
                        self._st())
-                L.call("nmfb_tc_gemm", vp(d.X), n, m, vp(Ft[0]), vp(Ft[1]), r,
-                       vp(self.ybuf), self.tc_req, 0, self._st())
+                if self.yt_out is None:
+                    L.call("nmfb_tc_gemm", vp(d.X), n, m, vp(Ft[0]), vp(Ft[1]), r,
+                           vp(self.ybuf), self.tc_req, 0, self._st())
+                else:
+                    # each owner's rows go straight into its receive buffer
+                    dst, world, chunk, src = self.yt_out
+                    L.call("nmfb_tc_gemm_rows", vp(d.X), n, m, vp(Ft[0]), vp(Ft[1]), r,
+                           self.tc_req, dst, world, chunk, src, self._st())
             elif self.mode == L.MODE_FAST:
                 L.call("nmfb_gemm_tall", vp(d.XT), 0, n, m, n, vp(self.FT), r, r,
                        vp(self.ybuf), self.splits_m, self._st())

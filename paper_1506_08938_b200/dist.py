@@ -22,6 +22,18 @@ needs all of G); the north star lists only the first two.
 The per-rank numerics come from an *engine* (the CUDA engine below for the
 product; tests/ plug an oracle engine in to check the sharding logic on CPU
 with gloo).  The driver itself does no arithmetic beyond summing scalars.
+
+Peer-memory path (dense fp32 on GPUs with peer access; the default when
+torch symmetric memory is available, NMFB_DIST_PEER=0 forces NCCL).  The
+exchanges above become stores issued by the producing kernels into the
+consumers' symmetric buffers over NVLink (PeerExchange, csrc/peer.cu):
+  X F^T GEMM epilogue  -> owner rank's Y^T receive slots    (reduce-scatter)
+  M-step NNLS epilogue -> every rank's copy of G            (all-gather)
+  F_g F_g^T, objective pieces -> per-source slots            (allreduce)
+with one epoch flag barrier after each producer and a fixed-order slot sum
+at the consumer, so every rank computes the same bits independent of any
+collective's reduction order.  G is then replicated exactly, so the Gram of
+G is computed locally (fused with its rescale) instead of allreduced.
 """
 
 from __future__ import annotations
@@ -61,6 +73,73 @@ class ShardPlan:
 
     def row_range(self, rank):
         return self.rows[rank]
+
+
+class PeerExchange:
+    """Symmetric device buffers shared by all ranks over NVLink + epoch flags.
+
+    One symmetric allocation (torch symmetric memory; its rendezvous hands out
+    every rank's mapping) carved into named regions; `ptrs(name)` lists the
+    region's address on every rank.  Flags: world epoch words (one per source
+    rank) + an error word, at the end of the allocation."""
+
+    ALIGN = 256
+
+    def __init__(self, regions, device, group=None, timeout_s=60.0):
+        import torch.distributed._symmetric_memory as symm
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > L.MAX_PEERS:
+            raise ValueError(f"peer exchange supports up to {L.MAX_PEERS} ranks")
+        gname = (group or dist.group.WORLD).group_name
+        self.offsets = {}
+        off = 0
+        for name, nbytes in list(regions.items()) + [("flags", 8 * (self.world + 1))]:
+            self.offsets[name] = (off, int(nbytes))
+            off += -(-int(nbytes) // self.ALIGN) * self.ALIGN
+        self.buf = symm.empty(max(off, self.ALIGN), dtype=torch.uint8, device=device)
+        self.buf.zero_()
+        self.handle = symm.rendezvous(self.buf, gname)
+        self.bases = [int(p) for p in self.handle.buffer_ptrs]
+        if len(self.bases) != self.world:
+            raise RuntimeError("symmetric memory rendezvous returned the wrong rank count")
+        self.ticket = torch.zeros((1,), dtype=torch.int32, device=device)
+        self.flag_ptrs = L.ptr_array(self.ptrs("flags"))
+        self.epoch = 0
+        self.timeout_s = float(timeout_s)
+        torch.cuda.synchronize(device)
+        dist.barrier(group)  # every rank's flags are zero before anyone signals
+
+    def ptrs(self, name, byte_offset=0):
+        off = self.offsets[name][0] + byte_offset
+        return [b + off for b in self.bases]
+
+    def view(self, name, dtype):
+        off, nbytes = self.offsets[name]
+        return self.buf[off: off + nbytes].view(dtype)
+
+    def put(self, src, name, byte_offset):
+        """Copy src (contiguous, 8-byte multiple) to region `name` at
+        byte_offset on every rank (no signal)."""
+        nbytes = src.numel() * src.element_size()
+        L.call("nmfb_peer_put", D.vp(src), nbytes, L.ptr_array(self.ptrs(name, byte_offset)),
+               self.world, self.rank, None, None, 0, 0, D.stream_handle())
+
+    def barrier(self):
+        """All writes this rank issued so far (kernels earlier on the stream)
+        are visible on every peer, and every peer's on this rank."""
+        self.epoch += 1
+        L.call("nmfb_peer_put", None, 0, None, self.world, self.rank, self.flag_ptrs,
+               D.vp(self.ticket), self.epoch, 1, D.stream_handle())
+        L.call("nmfb_peer_wait", self.ptrs("flags")[self.rank], self.world, self.epoch,
+               self.timeout_s, D.stream_handle())
+
+    def check(self):
+        """Raise if a wait timed out (synchronises)."""
+        err = int(self.view("flags", torch.int64)[self.world].item())
+        if err:
+            raise RuntimeError(f"peer exchange: wait for epoch {err} timed out")
 
 
 class DistAlternation:
@@ -116,6 +195,12 @@ class DistAlternation:
         e, p = self.e, self.plan
         rlo, rhi = p.row_range(self.rank)
         clo, chi = p.col_range(self.rank)
+        if getattr(e, "px", None) is not None:
+            # peer-memory path: the producers' stores are the exchanges
+            e.estep_peer(k, clo)
+            e.mstep_peer(k, rlo, rhi)
+            e.objective_peer(k, rlo, rhi)
+            return
         # Gram of G: partial over my rows, allreduced (first iteration: all rows
         # are already replicated, so every rank's partial covers its own block)
         Qg = self._allreduce(e.gram_rows(rlo, rhi))
@@ -216,6 +301,81 @@ class CudaEngine:
     def set_g(self, G_full):
         pass  # the allgather filled st.G's padded buffer in place
 
+    # -- peer-memory path -------------------------------------------------------
+    def enable_peer(self, plan, group=None):
+        """Move G and the exchange buffers into symmetric memory (all ranks
+        call this together).  Dense fp32 tensor-core path only."""
+        st, n, r = self.st, self.data.n, self.r
+        if not (self.ysplit and getattr(st, "use_tc", False)):
+            raise ValueError("the peer path needs the dense fp32 tensor-core engine")
+        world = plan.world
+        self.P = st.splits_m  # partial slots per rank (equal column blocks: same on every rank)
+        chunk = plan.row_chunk
+        regions = {
+            "yt": 4 * world * self.P * chunk * r,      # Y^T partial slots, by source rank
+            "g": 4 * plan.padded_rows * r,             # replicated G (row-blocked)
+            "hf": 8 * world * r * r,                   # F_g F_g^T by source rank
+            "pieces": 8 * world * st.max_iters * 12,   # objective pieces [src][k][12]
+        }
+        px = PeerExchange(regions, self.data.device, group)
+        g = px.view("g", torch.float32).view(plan.padded_rows, r)
+        g[:n].copy_(st.G)
+        st.G = g[:n]
+        self.g_pad = g
+        self.plan = plan
+        self.yt_recv = px.view("yt", torch.float32)
+        self.hf_slots = px.view("hf", torch.float64)
+        self.piece_slots = px.view("pieces", torch.float64)
+        st.yt_out = (L.ptr_array(px.ptrs("yt")), world, chunk, px.rank)
+        lo, hi = plan.row_range(px.rank)
+        self.g_mirror = L.ptr_array([q for i, q in enumerate(px.ptrs("g", lo * r * 4))
+                                     if i != px.rank])
+        self.n_mirror = world - 1
+        self.iters_done = 0
+        torch.cuda.synchronize()
+        px.barrier()
+        self.px = px
+
+    def estep_peer(self, k, col_offset):
+        st, px, r = self.st, self.px, self.r
+        st.index_base_e = col_offset
+        st.qg_valid = False  # G is replicated exactly: Gram + rescale locally
+        st.estep(k)          # the X F^T epilogue stores into the owners' slots
+        px.put(st.Hf, "hf", px.rank * r * r * 8)
+        px.barrier()
+        L.call("nmfb_sum_slots_f64", D.vp(self.hf_slots), px.world, r * r, r * r, D.vp(st.Hf),
+               D.stream_handle())
+        st.rescale(st.Hf, 2.0 * self.cfg.beta2, 1)
+
+    def mstep_peer(self, k, lo, hi):
+        st, px, r = self.st, self.px, self.r
+        if hi > lo:
+            L.call("nmfb_nnls_batch_peers", st.code, st.mode, D.vp(st.Qa[1]), D.vp(st.sa[1]),
+                   D.vp(st.act[1]), D.vp(st.active[1]), r, r, D.vp(st.ra[1]),
+                   D.vp(self.yt_recv), L.F32, px.world * self.P, r, self.plan.row_chunk * r,
+                   self.cfg.beta1, D.vp(st.G[lo:hi]), hi - lo, lo, float(self.cfg.epsilon),
+                   int(self.cfg.inner_cap), 0.0, None, None, D.vp(st.stats[k, 1]), st.lanes,
+                   self.g_mirror, self.n_mirror, D.stream_handle())
+        px.barrier()  # every rank now holds all of G
+
+    def objective_peer(self, k, lo, hi):
+        px = self.px
+        p = self.objective_pieces(k, None, lo, hi)
+        # slot [src][k]; summed once at finish() (slots are per iteration, so
+        # no barrier is needed here)
+        px.put(p, "pieces", (px.rank * self.st.max_iters + k) * 12 * 8)
+        self.iters_done = max(self.iters_done, k + 1)
+
+    def finish(self):
+        """Sum the objective-piece slots of every iteration run so far."""
+        px = getattr(self, "px", None)
+        if px is None or self.iters_done == 0:
+            return
+        px.barrier()
+        K = self.iters_done
+        L.call("nmfb_sum_slots_f64", D.vp(self.piece_slots), px.world, K * 12,
+               self.st.max_iters * 12, D.vp(self.st.pieces), D.stream_handle())
+
     def objective_pieces(self, k, yt_rows, lo, hi):
         """Additive per-rank pieces (slot layout of device.Alternation):
         dense residual over my columns; sparse cross <G[R], Y^T[R]> over my
@@ -272,9 +432,28 @@ class DistFit:
             raise ValueError("every rank must hold a 32-aligned equal column block")
         G0, FT0 = init
         self.engine = CudaEngine(X_block, cfg, G0, FT0, cfg.max_outer, m)
-        self.engine.bind_plan(self.plan)
+        self.peer = False
+        if peer_wanted(self.engine):
+            try:
+                self.engine.enable_peer(self.plan, group)
+                self.peer = True
+            except Exception as exc:  # no peer access / symmetric memory: NCCL
+                self.peer_error = f"{type(exc).__name__}: {exc}"
+        if not self.peer:
+            self.engine.bind_plan(self.plan)
         self.state = _StateView(DistAlternation(self.engine, self.plan, rank, group),
                                 self.engine.st)
+
+
+def peer_wanted(engine):
+    """Peer path: dense fp32 tensor-core engine, NCCL group, not disabled."""
+    import os
+
+    if os.environ.get("NMFB_DIST_PEER", "1") == "0":
+        return False
+    if not (dist.is_initialized() and dist.get_backend() == "nccl"):
+        return False
+    return bool(engine.ysplit and getattr(engine.st, "use_tc", False))
 
 
 class _StateView:
@@ -291,6 +470,9 @@ class _StateView:
         self.da.iterate(k)
 
     def join(self):
+        fin = getattr(self.da.e, "finish", None)
+        if fin is not None:
+            fin()
         self.st.join()
 
     def assemble(self, *a, **kw):
