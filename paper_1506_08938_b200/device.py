@@ -501,6 +501,45 @@ class Alternation:
                     self._wait_residual(q)
             torch.cuda.current_stream().wait_stream(main)
 
+    def snapshot(self):
+        """Copy G, F^T (the state after the last enqueued iteration) into
+        backup buffers, stream-ordered -- the lag-1 convergence check of
+        FitSession.run keeps launching while it inspects the previous
+        iteration, and rolls back if that one met the stopping rule."""
+        if getattr(self, "_bak", None) is None:
+            self._bak = (torch.empty_like(self.G), torch.empty_like(self.FT))
+        main = getattr(self, "main", None)
+        if main is not None:
+            main.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(main):
+                self._bak[0].copy_(self.G)
+                self._bak[1].copy_(self.FT)
+        else:
+            self._bak[0].copy_(self.G)
+            self._bak[1].copy_(self.FT)
+
+    def restore(self):
+        """G, F^T <- the last snapshot (after join())."""
+        self.G.copy_(self._bak[0])
+        self.FT.copy_(self._bak[1])
+
+    def done_event(self, k):
+        """An event on the caller's stream that completes when iteration k
+        (both steps and its objective pieces) is done, without making the
+        step streams wait."""
+        cur = torch.cuda.current_stream()
+        main = getattr(self, "main", None)
+        if main is not None:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            cur.wait_event(ev)
+            res = self.res_ev[k % 2]
+            if res is not None:
+                cur.wait_event(res)
+        done = torch.cuda.Event(enable_timing=True)
+        done.record(cur)
+        return done
+
     def iterate(self, k):
         main = getattr(self, "main", None)
         if main is None:

@@ -235,43 +235,25 @@ class FitSession:
 
     def run(self):
         cfg, st = self.cfg, self.state
+        # the stopping rule / callback need every objective on the host
         sync_each = cfg.rel_change_tol > 0.0 or self.on_iteration is not None
         start = torch.cuda.Event(enable_timing=True)
-        events = []
         log = ConvergenceLog()
         start.record()
-        previous = None
-        done = 0
         xsq = getattr(self.data, "xsq", 0.0)
         try:
-            for k in range(cfg.max_outer):
-                st.iterate(k)
-                if sync_each or k == cfg.max_outer - 1:
-                    st.join()
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record()
-                events.append(ev)
-                done = k + 1
-                if sync_each:
-                    ev.synchronize()
-                    stats = st.stats[k].cpu().numpy()
-                    err = st.failure(stats[None], 0)
-                    if err is not None:
-                        raise err
-                    pieces = st.pieces[k].cpu().numpy()
-                    obj = st.assemble(pieces, cfg, self.data.kind, xsq)
-                    log.append(obj, start.elapsed_time(ev) / 1e3, int(stats[:, 0].sum()),
-                               self.m + self.n)
-                    if self.on_iteration is not None:
-                        self.on_iteration(log)
-                    if (cfg.rel_change_tol > 0.0 and previous is not None
-                            and abs(previous - obj)
-                            <= cfg.rel_change_tol * max(abs(previous), 1e-300)):
-                        break
-                    previous = obj
-            if not sync_each:
+            if sync_each:
+                self._run_lagged(st, log, start, xsq)
+            else:
+                # fixed iteration count: launch everything, read the log once
+                events = []
+                for k in range(cfg.max_outer):
+                    st.iterate(k)
+                    events.append(st.done_event(k))
                 st.join()
-                events[-1].synchronize()
+                done = len(events)
+                if done:
+                    events[-1].synchronize()
                 stats = st.stats[:done].cpu().numpy()
                 pieces = st.pieces[:done].cpu().numpy()
                 for k in range(done):
@@ -287,6 +269,52 @@ class FitSession:
         G, FT = st.factors_host()
         model = NmfModel(G=DenseMatrix(G), F=DenseMatrix(np.asfortranarray(FT.T)))
         return model, log
+
+    def _check(self, st, log, k, ev, start, xsq, previous):
+        """Host-side bookkeeping of iteration k (nmf.py:193-206) once its
+        event is done: failure, log entry, callback, stopping rule.  Returns
+        (stop, objective)."""
+        cfg = self.cfg
+        ev.synchronize()
+        stats = st.stats[k].cpu().numpy()
+        err = st.failure(stats[None], 0)
+        if err is not None:
+            raise err
+        obj = st.assemble(st.pieces[k].cpu().numpy(), cfg, self.data.kind, xsq)
+        log.append(obj, start.elapsed_time(ev) / 1e3, int(stats[:, 0].sum()), self.m + self.n)
+        if self.on_iteration is not None:
+            self.on_iteration(log)
+        stop = (cfg.rel_change_tol > 0.0 and previous is not None
+                and abs(previous - obj) <= cfg.rel_change_tol * max(abs(previous), 1e-300))
+        return stop, obj
+
+    def _run_lagged(self, st, log, start, xsq):
+        """Per-iteration convergence check without a per-iteration stall:
+        iteration k+1 is enqueued before the host inspects iteration k (the
+        objective needs a device->host read).  A snapshot of (G, F) taken
+        before k+1 lets the fit return exactly the state after k when k met
+        the stopping rule -- the same result as the synchronous loop."""
+        cfg = self.cfg
+        pending = None  # (k, event)
+        previous = None
+        for k in range(cfg.max_outer):
+            if pending is not None:
+                st.snapshot()  # state after iteration k - 1
+            st.iterate(k)
+            if pending is not None:
+                # inspect k - 1 while k runs; the caller's stream has no wait
+                # on iteration k queued yet, so the reads do not stall on it
+                stop, previous = self._check(st, log, pending[0], pending[1], start, xsq,
+                                             previous)
+                if stop:
+                    st.join()
+                    st.restore()
+                    return pending[0] + 1
+            pending = (k, st.done_event(k))
+        if pending is not None:
+            self._check(st, log, pending[0], pending[1], start, xsq, previous)
+        st.join()
+        return cfg.max_outer
 
 
 def fit(V, cfg, on_iteration=None):

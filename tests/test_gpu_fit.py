@@ -322,3 +322,33 @@ def test_fit_rejects_bad_data(bad, as_torch):
     V = torch.from_numpy(x) if as_torch else x
     with pytest.raises(DataDomainError):
         fit(V, NmfConfig(rank=4, max_outer=2, precision="fp32"))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_lagged_convergence_check_returns_the_stopping_iterate(precision):
+    """The per-iteration stopping rule is checked one iteration behind the
+    launches (no per-iteration stall); the model must still be the state after
+    the iteration that met the rule: identical to a fixed-count fit of that
+    many iterations, and the log identical too."""
+    X = FITS["planted/X"]
+    model, log = _fit(X, precision, rank=4, max_outer=300, seed=1, rel_change_tol=0.05)
+    K = len(log)
+    assert 2 < K < 300
+    ref_model, ref_log = _fit(X, precision, rank=4, max_outer=K, seed=1, rel_change_tol=0.0)
+    assert np.array_equal(model.G.array, ref_model.G.array)
+    assert np.array_equal(model.F.array, ref_model.F.array)
+    assert log.objective == ref_log.objective
+    assert log.inner_iterations == ref_log.inner_iterations
+
+
+def test_on_iteration_callback_sees_every_iteration():
+    from paper_1506_08938_b200 import NmfConfig, fit
+
+    seen = []
+    X = FITS["planted/X"]
+    cfg = NmfConfig(precision="fp32", rank=4, max_outer=7, seed=1, rel_change_tol=0.0)
+    model, log = fit(X, cfg, on_iteration=lambda lg: seen.append(len(lg)))
+    assert seen == list(range(1, 8))
+    ref_model, ref_log = _fit(X, "fp32", rank=4, max_outer=7, seed=1, rel_change_tol=0.0)
+    assert np.array_equal(model.G.array, ref_model.G.array)
+    assert log.objective == ref_log.objective
