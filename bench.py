@@ -68,18 +68,37 @@ def make_block(rank):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+    """SM clock + throttle reasons sampled DURING the timed region (the
+    recipe's clocks line): NVML polled every ~1 ms from a thread while the
+    steps run (nvidia-smi's 100 ms loop would miss a 15 ms region); falls back
+    to nvidia-smi if NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.halt = False
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -90,11 +109,30 @@ class Clocks:
         except OSError:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.halt:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self):
+        if self.nvml is not None:
+            self.halt = True
+            self.thread.join(timeout=2)
+            sm = [float(r[0]) for r in self.rows]
+            reasons = sorted({nm for _, rs in self.rows for nm, bit in self.REASONS if rs & bit})
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": float(self.max_sm), "reasons": reasons,
+                    "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -114,7 +152,7 @@ class Clocks:
                         reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 def peaks():
@@ -162,8 +200,10 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     X = make_block(rank)
     n, m = X.shape
-    cfg = NmfConfig(rank=RANK, max_outer=args.warmup + args.steps, seed=SEED, rel_change_tol=0.0,
-                    precision="fp32")
+    # iteration slots: warm-up, the timed steps, then the same number of
+    # instrumented steps (per-kernel CUDA events) for the kernel shares
+    cfg = NmfConfig(rank=RANK, max_outer=args.warmup + 2 * args.steps, seed=SEED,
+                    rel_change_tol=0.0, precision="fp32")
     G0, FT0 = initial_factors_from_mean(n, m * world, float(X.mean()), cfg)
     FT0 = FT0[rank * m:(rank + 1) * m]
     if use_dist:
@@ -189,7 +229,10 @@ def run_ours(args):
     clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with _lib.Recorder(timing=True) as rec:
+    # timed steps: launch counting, and CUDA events around the dominant
+    # (data-product GEMM) calls only -- the roofline's live launch durations
+    gemm_names = {"nmfb_tc_gemm", "nmfb_tc_gemm_rows", "nmfb_gemm_tall"}
+    with _lib.Recorder(timing=gemm_names) as cnt:
         t0.record()
         for k in range(args.warmup, args.warmup + args.steps):
             st.iterate(k)
@@ -198,6 +241,19 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
+    # the same number of steps again with a CUDA event pair around every
+    # C-ABI call: per-kernel durations and shares (the events add small gaps,
+    # so these steps are not the timed ones)
+    with _lib.Recorder(timing=True) as rec:
+        i0 = torch.cuda.Event(enable_timing=True)
+        i1 = torch.cuda.Event(enable_timing=True)
+        i0.record()
+        for k in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+            st.iterate(k)
+        st.join()
+        i1.record()
+    torch.cuda.synchronize()
+    ms_instr = i0.elapsed_time(i1)
     if use_dist:
         tt = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -210,9 +266,10 @@ def run_ours(args):
     dom = max(calls.items(), key=lambda kv: kv[1][1])
     hbm, peak_src = peaks()
     gname = "nmfb_tc_gemm" if "nmfb_tc_gemm" in calls else "nmfb_gemm_tall"
-    gemm_calls, gemm_ms = calls.get(gname, (0, 0.0))
-    if "nmfb_tc_gemm_rows" in calls:  # multi-GPU peer path: X F^T stores into the owners
-        c2, t2 = calls["nmfb_tc_gemm_rows"]
+    live = cnt.summary()  # GEMM launches inside the timed region
+    gemm_calls, gemm_ms = live.get(gname, (0, 0.0))
+    if "nmfb_tc_gemm_rows" in live:  # multi-GPU peer path: X F^T stores into the owners
+        c2, t2 = live["nmfb_tc_gemm_rows"]
         gemm_calls, gemm_ms = gemm_calls + c2, gemm_ms + t2
     # algorithmic bytes per data-product launch, averaged over the two passes
     # (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once, B^T hi+lo, split-K C
@@ -222,11 +279,11 @@ def run_ours(args):
     achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9 if gemm_avg_ms > 0 else 0.0
     kernels = {}
     for name, (c, t) in calls.items():
-        kernels[name] = {"launches": c, "avg_ms": t / c, "share": round(t / ms, 4)}
+        kernels[name] = {"launches": c, "avg_ms": t / c, "share": round(t / ms_instr, 4)}
     if "nmfb_dense_residual_kmajor" in calls:
         c, t = calls["nmfb_dense_residual_kmajor"]
         kernels["nmfb_dense_residual_kmajor"]["fp32_tflops"] = 2.0 * n * m * RANK / (t / c / 1e3) / 1e12
-    share = {k: round(v[1] / ms, 4) for k, v in calls.items()}
+    share = {k: round(v[1] / ms_instr, 4) for k, v in calls.items()}
     # log sanity: objective decreasing
     pieces = st.pieces[: args.warmup + args.steps].cpu().numpy()
     objs = [st.assemble(p, cfg, "dense", 0.0) for p in pieces]
@@ -263,7 +320,8 @@ def run_ours(args):
         "kernels": kernels,
         "dominant": dom[0],
         "clocks": clk,
-        "gpu_launches": rec.launches,
+        "gpu_launches": cnt.launches,
+        "instrumented_ms_per_step": ms_instr / args.steps,
         "objective_first_last": [objs[0], objs[-1]],
     }
     if rank == 0 and world == 1 and not args.no_e2e:

@@ -162,6 +162,7 @@ class Recorder:
     active = None
 
     def __init__(self, timing=False):
+        # timing: True (every call), False, or a set of entry-point names
         self.timing = timing
         self.launches = 0
         self.calls = []  # (name, start_event, end_event)
@@ -186,7 +187,7 @@ def call(name, *args):
     rec = Recorder.active
     if rec is not None:
         rec.launches += KERNELS_PER_CALL.get(name, 0)
-        if rec.timing:
+        if rec.timing is True or (rec.timing and name in rec.timing):
             import torch
 
             a = torch.cuda.Event(enable_timing=True)
