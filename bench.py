@@ -39,6 +39,15 @@ sys.path.insert(0, REPO)
 
 N_ROWS, N_COLS, RANK, SEED = 10000, 20000, 50, 1
 WORKLOAD = "C2: dense NMF 10000x20000, rank 50, fp32 (BASELINE.json configs[1])"
+WORKLOADS = {
+    2: WORKLOAD,
+    3: "C3: sparse text-like NMF 100000x50000 CSC 0.1%, rank 100, fp32 (BASELINE.json configs[2])",
+    4: "C4: dense L1/L2-regularised NMF 20000x20000, rank 64, mu1=0.1, beta2=0.01, fp32 "
+       "(BASELINE.json configs[3])",
+    5: "C5: sparse text-like NMF 1000000x200000 CSC 0.05%, rank 200, fp32 (BASELINE.json "
+       "configs[4]), single-GPU leg",
+}
+FP32_TFLOPS = 148 * 128 * 2 * 1965e6 / 1e12  # FFMA peak from the measured max SM clock
 
 
 def parse():
@@ -49,6 +58,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                   help="BASELINE.json config (default 2 = configs[1], the headline workload); "
+                        "3-5 are measured here too (sparse 3/5 at N = 1)")
     return p.parse_args()
 
 
@@ -59,12 +71,26 @@ def dist_env():
     return world, rank, local
 
 
-def make_block(rank):
-    """This rank's C2-shaped column block (float64 host, (n, m) Fortran)."""
+def make_block(rank, cid=2):
+    """This rank's column block: dense configs are weak-scaled (every rank a
+    config-shaped block, seeds differ per rank; float64 host, (n, m) Fortran);
+    sparse configs are the config's full CSC (N = 1)."""
     from oracle import generators
 
+    c = generators.CONFIGS[cid]
+    if c["kind"] == "sparse":
+        x, _ = generators.make(cid)
+        return x
+    n, m = c["shape"]
     seed = SEED if rank == 0 else SEED + 1000 * rank
-    return np.asfortranarray(generators.dense_exp(N_ROWS, N_COLS, RANK, 0.05, seed))
+    return np.asfortranarray(generators.dense_exp(n, m, c["rank"], 0.05, seed))
+
+
+def config_knobs(cid):
+    """NmfConfig keywords of a BASELINE config (rank, seed, penalties)."""
+    from oracle import generators
+
+    return dict(generators.CONFIGS[cid]["cfg"])
 
 
 class Clocks:
@@ -184,6 +210,16 @@ def profile_traffic(kernel="nmfb_tc_gemm"):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def st_inner(st, k0, k1):
+    """Inner NNLS iterations of steps [k0, k1) from the device stats."""
+    stats = getattr(st, "stats", None)
+    if stats is None:
+        stats = getattr(getattr(st, "st", None), "stats", None)
+    if stats is None:
+        return 0
+    return int(stats[k0:k1, :, 0].sum().item())
+
+
 def run_ours(args):
     import torch
 
@@ -198,13 +234,27 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    X = make_block(rank)
-    n, m = X.shape
+    cid = args.config
+    X = make_block(rank, cid)
+    sparse = not isinstance(X, np.ndarray)
+    if sparse and world > 1:
+        raise SystemExit("bench.py: sparse configs are measured at N = 1 (see DESIGN.md)")
+    if sparse:
+        from paper_1506_08938_b200.matrix import SparseMatrix
+
+        X = SparseMatrix(X.rows, X.cols, X.indptr, X.indices, X.values, validate=False)
+        n, m = X.rows, X.cols
+        xmean = float(X.values.sum()) / (n * m)
+    else:
+        n, m = X.shape
+        xmean = float(X.mean())
+    knobs = config_knobs(cid)
+    R = knobs["rank"]
     # iteration slots: warm-up, the timed steps, then the same number of
     # instrumented steps (per-kernel CUDA events) for the kernel shares
-    cfg = NmfConfig(rank=RANK, max_outer=args.warmup + 2 * args.steps, seed=SEED,
-                    rel_change_tol=0.0, precision="fp32")
-    G0, FT0 = initial_factors_from_mean(n, m * world, float(X.mean()), cfg)
+    cfg = NmfConfig(max_outer=args.warmup + 2 * args.steps, rel_change_tol=0.0,
+                    precision="fp32", **knobs)
+    G0, FT0 = initial_factors_from_mean(n, m * world, xmean, cfg)
     FT0 = FT0[rank * m:(rank + 1) * m]
     if use_dist:
         from paper_1506_08938_b200 import dist as PD
@@ -231,7 +281,8 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     # timed steps: launch counting, and CUDA events around the dominant
     # (data-product GEMM) calls only -- the roofline's live launch durations
-    gemm_names = {"nmfb_tc_gemm", "nmfb_tc_gemm_rows", "nmfb_gemm_tall"}
+    gemm_names = {"nmfb_tc_gemm", "nmfb_tc_gemm_rows", "nmfb_gemm_tall", "nmfb_csc_linear",
+                  "nmfb_csr_yt_chunked"}
     with _lib.Recorder(timing=gemm_names) as cnt:
         t0.record()
         for k in range(args.warmup, args.warmup + args.steps):
@@ -259,34 +310,77 @@ def run_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
     ms_per_step = ms / args.steps
-    solves_step = (m * world + n)
+    solves_step = (m * world + n)  # per step, all ranks
     value = solves_step * args.steps / (ms / 1e3)
     calls = rec.summary()
     # dominant kernel: the largest share of the step
     dom = max(calls.items(), key=lambda kv: kv[1][1])
     hbm, peak_src = peaks()
-    gname = "nmfb_tc_gemm" if "nmfb_tc_gemm" in calls else "nmfb_gemm_tall"
-    live = cnt.summary()  # GEMM launches inside the timed region
-    gemm_calls, gemm_ms = live.get(gname, (0, 0.0))
-    if "nmfb_tc_gemm_rows" in live:  # multi-GPU peer path: X F^T stores into the owners
-        c2, t2 = live["nmfb_tc_gemm_rows"]
-        gemm_calls, gemm_ms = gemm_calls + c2, gemm_ms + t2
-    # algorithmic bytes per data-product launch, averaged over the two passes
-    # (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once, B^T hi+lo, split-K C
-    se, sm = getattr(st, "splits_e", 1), getattr(st, "splits_m", 1)
-    gemm_bytes = 4.0 * (n * m + RANK * (n + m) + (se * m + sm * n) * RANK / 2.0)
-    gemm_avg_ms = gemm_ms / max(gemm_calls, 1)
-    achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9 if gemm_avg_ms > 0 else 0.0
+    live = cnt.summary()  # data-product launches inside the timed region
     kernels = {}
     for name, (c, t) in calls.items():
         kernels[name] = {"launches": c, "avg_ms": t / c, "share": round(t / ms_instr, 4)}
-    if "nmfb_dense_residual_kmajor" in calls:
-        c, t = calls["nmfb_dense_residual_kmajor"]
-        kernels["nmfb_dense_residual_kmajor"]["fp32_tflops"] = 2.0 * n * m * RANK / (t / c / 1e3) / 1e12
     share = {k: round(v[1] / ms_instr, 4) for k, v in calls.items()}
+    # inner iterations of the timed steps -> k-bar for the NNLS flop count
+    inner = st_inner(st, args.warmup, args.warmup + args.steps)
+    kbar = inner / (solves_step * world * args.steps) if inner else 1.0
+    rooflines = {}
+    if not sparse:
+        gname = "nmfb_tc_gemm" if "nmfb_tc_gemm" in calls else "nmfb_gemm_tall"
+        gemm_calls, gemm_ms = live.get(gname, (0, 0.0))
+        if "nmfb_tc_gemm_rows" in live:  # multi-GPU peer path: X F^T stores into the owners
+            c2, t2 = live["nmfb_tc_gemm_rows"]
+            gemm_calls, gemm_ms = gemm_calls + c2, gemm_ms + t2
+        # algorithmic bytes per data-product launch, averaged over the two passes
+        # (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once, B^T hi+lo, split-K C
+        se, sm = getattr(st, "splits_e", 1), getattr(st, "splits_m", 1)
+        gemm_bytes = 4.0 * (n * m + R * (n + m) + (se * m + sm * n) * R / 2.0)
+        gemm_avg_ms = gemm_ms / max(gemm_calls, 1)
+        achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9 if gemm_avg_ms > 0 else 0.0
+        rooflines["data_products"] = {
+            "kernel": gname + " (G^T X and X F^T passes over X; tcgen05 3xTF32)",
+            "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": gemm_bytes, "avg_launch_ms": gemm_avg_ms,
+            "timed": "live CUDA events in the timed steps", "traffic": profile_traffic()}
+    else:
+        # compulsory bytes of one SpMM pass: values + indices once,
+        # the pointer array, both factors read/written once
+        nnz = X.nnz
+        sp_bytes = 8.0 * nnz + 8.0 * (m + 1) + 4.0 * (n + m) * R
+        sp_calls = sum(live.get(k, (0, 0.0))[0] for k in ("nmfb_csc_linear", "nmfb_csr_yt_chunked"))
+        sp_ms = sum(live.get(k, (0, 0.0))[1] for k in ("nmfb_csc_linear", "nmfb_csr_yt_chunked"))
+        sp_avg = sp_ms / max(sp_calls, 1)
+        ach = sp_bytes / (sp_avg / 1e3) / 1e9 if sp_avg > 0 else 0.0
+        rooflines["data_products"] = {
+            "kernel": "nmfb_csc_linear + nmfb_csr_yt_chunked (G^T X and X F^T, CSC / CSR SpMM)",
+            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": sp_bytes,
+            "avg_launch_ms": sp_avg, "timed": "live CUDA events in the timed steps",
+            "gather_bytes_per_launch": 4.0 * nnz * R,
+            "note": "compulsory bytes; the factor-row gathers (gather_bytes) are served "
+                    "by L2 when the factor fits (C3), by HBM when it does not (C5)"}
+    if "nmfb_nnls_batch" in calls:
+        c, t = calls["nmfb_nnls_batch"]
+        # 2 r^2 (1 + 2 k) flops per solve (gradient init, Q d per
+        # inner iteration, r coordinate-descent column updates per iteration)
+        fl = 2.0 * R * R * (1 + 2 * kbar) * (m + n / world)  # this rank's solves
+        nn_ms = t / (c / 2)  # both NNLS launches of one step
+        ach = fl / (nn_ms / 1e3) / 1e12
+        rooflines["nnls"] = {
+            "kernel": "nmfb_nnls_batch (E + M solves of one step)", "bound": "fp32",
+            "achieved": ach, "peak": FP32_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP32_TFLOPS,
+            "peak_source": "spec-derived: 148 SM x 128 FFMA lanes x 2 x measured max SM clock",
+            "algorithmic_flops_per_step": fl, "k_bar": kbar, "ms_per_step": nn_ms,
+            "timed": "instrumented steps (CUDA events around each call)",
+            "note": "counts FMAs only; the greedy-CD argmax scans (r compares per "
+                    "selection) are not counted, so this understates issued work"}
+    dominant_roof = rooflines["data_products"] if not sparse else \
+        max(rooflines.values(), key=lambda rf: rf.get("avg_launch_ms", rf.get("ms_per_step", 0)))
     # log sanity: objective decreasing
     pieces = st.pieces[: args.warmup + args.steps].cpu().numpy()
-    objs = [st.assemble(p, cfg, "dense", 0.0) for p in pieces]
+    xsq = X.sum_squares() if sparse else 0.0
+    objs = [st.assemble(p, cfg, "sparse" if sparse else "dense", xsq) for p in pieces]
     result = {
         "metric": "column NNLS solves/sec (NMF outer iteration: E+M steps + objective)",
         "value": value,
@@ -300,22 +394,21 @@ def run_ours(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "fp32",
-        "data": "synthetic (seeded generator oracle/generators.py, BASELINE C2 shape)",
-        "config": {"workload": WORKLOAD, "n": n, "m_per_gpu": m, "rank": RANK,
+        "data": f"synthetic (seeded generator oracle/generators.py, BASELINE C{cid} shape)",
+        "config": {"workload": WORKLOADS[cid], "n": n, "m_per_gpu": m, "rank": R,
                    "solves_per_step": solves_step,
                    "step": "one outer iteration of fit(): gram+rescale, G^T X, NNLS(m cols), "
                            "F F^T, X F^T, NNLS(n rows), objective",
-                   "l2": "inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
-                         % (n * m * 4 / 1e6),
+                   "l2": ("inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
+                          % (n * m * 4 / 1e6)) if not sparse else
+                         ("inputs larger than L2 (CSC + CSR of X = %.0f MB, factors %.0f MB)"
+                          % (16 * X.nnz / 1e6, 4 * (n + m) * R / 1e6)),
                    "parallelism": f"dp{world} (column-sharded)",
                    "exchange": ("nvlink peer stores from the producing kernels"
                                 if getattr(sess, "peer", False) else
                                 ("nccl" if use_dist else "none"))},
-        "roofline": {"kernel": gname + " (G^T X and X F^T passes over X; tcgen05 3xTF32)",
-                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": gemm_bytes,
-                     "avg_launch_ms": gemm_avg_ms, "traffic": profile_traffic()},
+        "roofline": dominant_roof,
+        "rooflines": rooflines,
         "step_share": share,
         "kernels": kernels,
         "dominant": dom[0],
@@ -326,7 +419,7 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_e2e:
         result["e2e"] = run_e2e(args, X, cfg)
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and cid == 2:
         result["cpu_baseline"] = cpu_baseline(X, bounded=True)
     if use_dist:
         torch.distributed.destroy_process_group()
@@ -334,29 +427,40 @@ def run_ours(args):
 
 
 def run_e2e(args, X, cfg):
-    """Public fit() from a pinned host buffer: H2D of X, init, K iterations,
-    D2H of factors and log, all inside the timed region."""
+    """Public fit() from host buffers: H2D of X (pinned fp32 for dense; the
+    SparseMatrix's CSC arrays for sparse, whose CSR twin is built on the
+    host), seeded init, K iterations, D2H of factors and log, all inside the
+    timed region."""
     import torch
 
     from paper_1506_08938_b200 import NmfConfig, fit
+    from paper_1506_08938_b200.matrix import SparseMatrix
 
-    n, m = X.shape
-    XT = torch.from_numpy(np.ascontiguousarray(X.T, dtype=np.float32)).pin_memory()
-    V = XT.t()  # (n, m) view of the pinned (m, n) buffer
-    ecfg = NmfConfig(rank=RANK, max_outer=args.steps, seed=SEED, rel_change_tol=0.0,
-                     precision="fp32")
-    fit(V, NmfConfig(rank=RANK, max_outer=2, seed=SEED, rel_change_tol=0.0, precision="fp32"))
+    knobs = config_knobs(args.config)
+    R = knobs["rank"]
+    if isinstance(X, SparseMatrix):
+        n, m = X.rows, X.cols
+        V = X
+        h2d = 8 * (m + 1) + 12 * X.nnz + 8 * (n + 1) + 12 * X.nnz + (n + m) * R * 4
+        call = f"fit(SparseMatrix CSC host arrays, max_outer={args.steps})"
+    else:
+        n, m = X.shape
+        XT = torch.from_numpy(np.ascontiguousarray(X.T, dtype=np.float32)).pin_memory()
+        V = XT.t()  # (n, m) view of the pinned (m, n) buffer
+        h2d = n * m * 4 + (n + m) * R * 4
+        call = f"fit(pinned torch (n,m) fp32 view, max_outer={args.steps})"
+    ecfg = NmfConfig(max_outer=args.steps, rel_change_tol=0.0, precision="fp32", **knobs)
+    warm = dict(knobs)
+    fit(V, NmfConfig(max_outer=2, rel_change_tol=0.0, precision="fp32", **warm))
     torch.cuda.synchronize()
     t = time.perf_counter()
     model, log = fit(V, ecfg)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
-    h2d = n * m * 4 + (n + m) * RANK * 4
-    d2h = (n + m) * RANK * 8 + args.steps * (12 * 8 + 4 * 8)
+    d2h = (n + m) * R * 8 + args.steps * (12 * 8 + 4 * 8)
     return {"value": (n + m) * args.steps / dt, "unit": "solves/s",
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-            "seconds": dt, "call": f"fit(pinned torch (n,m) fp32 view, max_outer={args.steps})",
-            "final_objective": log.final_objective}
+            "seconds": dt, "call": call, "final_objective": log.final_objective}
 
 
 # ---------------------------------------------------------------------------

@@ -32,6 +32,8 @@ int fast_launch_l1(const NnlsLaunch &p, int E, bool h64);
 int fast_launch_l2(const NnlsLaunch &p, int E, bool h64);
 int fast_launch_l4(const NnlsLaunch &p, int E, bool h64);
 int fast_launch_l8(const NnlsLaunch &p, int E, bool h64);
+int fast_pick_lx(int code, int need);
+int fast_launch_lx(const NnlsLaunch &p, int code, int E, bool h64);
 
 static int launch_fast(const NnlsLaunch &p) {
     // with a device-side ra the variant must cover the full rank r
@@ -45,7 +47,7 @@ static int launch_fast(const NnlsLaunch &p) {
         case 2: E = fast_pick_l2(need); return E ? fast_launch_l2(p, E, h64) : NMFB_ERR_ARG;
         case 4: E = fast_pick_l4(need); return E ? fast_launch_l4(p, E, h64) : NMFB_ERR_ARG;
         case 8: E = fast_pick_l8(need); return E ? fast_launch_l8(p, E, h64) : NMFB_ERR_ARG;
-        default: return NMFB_ERR_ARG;
+        default: E = fast_pick_lx(L, need); return E ? fast_launch_lx(p, L, E, h64) : NMFB_ERR_ARG;
     }
 }
 

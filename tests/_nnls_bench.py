@@ -6,8 +6,14 @@ from paper_1506_08938_b200 import NmfConfig, _lib as L
 from paper_1506_08938_b200 import device as D
 from paper_1506_08938_b200.nmf import FitSession
 from paper_1506_08938_b200.matrix import DenseMatrix
-cfgid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-x, cfg = generators.make(cfgid)
+cfgid = sys.argv[1] if len(sys.argv) > 1 else "2"
+if ":" in cfgid:  # custom sparse shape n:m:density:rank
+    n_, m_, dens_, r_ = cfgid.split(":")
+    x = generators.sparse_zipf(int(n_), int(m_), float(dens_), 5)
+    from oracle.nmf_oracle import Config
+    cfg = Config(rank=int(r_), seed=5, max_outer=8, rel_change_tol=0.0)
+else:
+    x, cfg = generators.make(int(cfgid))
 from paper_1506_08938_b200.matrix import SparseMatrix
 V = DenseMatrix(x) if isinstance(x, np.ndarray) else SparseMatrix(x.rows, x.cols, x.indptr, x.indices, x.values, validate=False)
 kw = dict(cfg.__dict__); kw.pop('workers'); kw['max_outer'] = 8
