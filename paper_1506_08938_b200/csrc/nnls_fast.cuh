@@ -28,18 +28,58 @@ __device__ __forceinline__ bool gany(bool p, unsigned gmask, int gbase) {
     return ((b >> gbase) & ((L == 32) ? 0xffffffffu : ((1u << L) - 1u))) != 0u;
 }
 
-// acc[e] += sum_j Q[k_e, j] * src_j, src_j owned by lane (j % L), element j / L.
-template <int E, int L>
-__device__ __forceinline__ void q_times(float (&acc)[E], const float (&src)[E], const float *Qrow,
-                                        int S, unsigned gmask) {
+// Shared-memory layout of the compact Q (ra x ra, symmetric), permuted per
+// row so that a lane's E coordinates are contiguous: row j holds, for lane
+// l, the entries Q[j][e*L + l] (e = 0..E-1) at Qs[j*SP + l*LS + e], LS = E
+// rounded up to 4 (zero padded) and then to an odd number of 16-byte quads,
+// SP = L*LS.  Both consumers read whole rows with 16-byte loads: the product
+// Q*src (all groups of a warp read the same row j -> broadcast) and the
+// greedy-CD gradient update with column p (= row p by symmetry).  With LS/4
+// odd, the 8 lanes of a quarter-warp start on 8 distinct bank quads:
+// conflict-free.
+__host__ __device__ constexpr int nnls_ep(int E) { return (E + 3) & ~3; }
+__host__ __device__ constexpr int nnls_ls(int E) {
+    return ((nnls_ep(E) / 4) & 1) ? nnls_ep(E) : nnls_ep(E) + 4;
+}
+__host__ __device__ constexpr int nnls_ee(int E) { return (E + 1) & ~1; }
+
+// acc[e] += s * row[e] for e < EE (EE = E rounded up to even), packed FFMA2.
+template <int EE, int EP>
+__device__ __forceinline__ void axpy_row(float (&acc)[EE], const float *row, float s) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    const float2 s2 = make_float2(s, s);
+#pragma unroll
+    for (int q = 0; q < EP / 4; ++q) {
+        const float4 v = r4[q];
+        if (4 * q + 1 < EE) {
+            const float2 o = __ffma2_rn(make_float2(v.x, v.y), s2,
+                                        make_float2(acc[4 * q], acc[4 * q + 1]));
+            acc[4 * q] = o.x;
+            acc[4 * q + 1] = o.y;
+        }
+        if (4 * q + 3 < EE) {
+            const float2 o = __ffma2_rn(make_float2(v.z, v.w), s2,
+                                        make_float2(acc[4 * q + 2], acc[4 * q + 3]));
+            acc[4 * q + 2] = o.x;
+            acc[4 * q + 3] = o.y;
+        }
+    }
+}
+
+// acc[e] += sum_j Q[k_e, j] * src(j), src(j) owned by lane (j % L), element
+// j / L; the source values come from a functor of the element index (held or
+// recomputed: d = passive gradient, delta = step).
+template <int E, int L, int EE, int EP, typename F>
+__device__ __forceinline__ void q_times_f(float (&acc)[EE], F src, const float *Qs_l,
+                                          unsigned gmask) {
+    constexpr int SP = L * nnls_ls(E);
 #pragma unroll 1
     for (int jl = 0; jl < L; ++jl) {
 #pragma unroll
         for (int je = 0; je < E; ++je) {
-            float sj = (L == 1) ? src[je] : __shfl_sync(gmask, src[je], jl, L);
-            const int jcol = je * L + jl;
-#pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = fmaf(Qrow[e * L * S + jcol], sj, acc[e]);
+            const float mine = src(je);
+            const float sj = (L == 1) ? mine : __shfl_sync(gmask, mine, jl, L);
+            axpy_row<EE, EP>(acc, Qs_l + (je * L + jl) * SP, sj);
         }
     }
 }
@@ -62,24 +102,6 @@ __device__ __forceinline__ float fast_h(const NnlsArgs<float, TH> &a, int64_t j,
     return (float)((TH)a.h_base - ((s0 + s1) + (s2 + s3)));
 }
 
-// Same, with the source values produced by a functor of the element index
-// (recomputed instead of held in registers: d = passive gradient, delta = step).
-template <int E, int L, typename F>
-__device__ __forceinline__ void q_times_f(float (&acc)[E], F src, const float *Qrow, int S,
-                                          unsigned gmask) {
-#pragma unroll 1
-    for (int jl = 0; jl < L; ++jl) {
-#pragma unroll
-        for (int je = 0; je < E; ++je) {
-            const float mine = src(je);
-            const float sj = (L == 1) ? mine : __shfl_sync(gmask, mine, jl, L);
-            const int jcol = je * L + jl;
-#pragma unroll
-            for (int e = 0; e < E; ++e) acc[e] = fmaf(Qrow[e * L * S + jcol], sj, acc[e]);
-        }
-    }
-}
-
 // Occupancy target: ~4E + 48 live registers per thread (y, grad and Q*d per
 // coordinate; the passive gradient and step are recomputed) -> CTAs per SM.
 __host__ __device__ constexpr int nnls_regs(int E, int L) { return 4 * E + 48 + (L == 1 ? 48 : 0); }
@@ -94,18 +116,24 @@ template <typename TH, int E, int L, int B, bool MIRROR>
 __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     nnls_fast_kernel(NnlsArgs<float, TH> a) {
     constexpr int R = E * L;
-    constexpr int S = R | 1;
+    constexpr int EE = nnls_ee(E), EP = nnls_ep(E), LS = nnls_ls(E), SP = L * LS;
     extern __shared__ __align__(16) float smem_f[];
-    float *Qs = smem_f;                          // R x S
+    float *Qs = smem_f;                          // R x SP, permuted rows (see nnls_ep)
     __shared__ float blk_norm[B][32], blk_final[B][32];
     __shared__ int blk_status[B][32];
     __shared__ int blk_any[B];
 
     const int tid = threadIdx.x;
     const int ra = a.ra_dev ? *a.ra_dev : a.ra, r = a.r;
-    for (int idx = tid; idx < R * S; idx += blockDim.x) {
-        int k = idx / S, c = idx - k * S;
-        Qs[idx] = (k < ra && c < ra) ? a.Qa[k * ra + c] : 0.0f;
+    {
+        float4 *q4 = reinterpret_cast<float4 *>(Qs);
+        for (int idx = tid; idx < R * SP / 4; idx += blockDim.x)
+            q4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        // coalesced reads of the compact Q, scattered into the permuted rows
+        for (int row = tid >> 5; row < ra; row += blockDim.x >> 5)
+            for (int k = tid & 31; k < ra; k += 32)
+                Qs[row * SP + (k % L) * LS + k / L] = a.Qa[row * ra + k];
     }
     __syncthreads();
 
@@ -122,9 +150,16 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     const int64_t j = g - a.index_base;
     const bool valid = blk_live && (g >= a.index_base) && (j < a.count);
     const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
-    const float *Qrow = Qs + l * S;  // row of coordinate e is Qrow + e*L*S
+    const float *Qsl = Qs + l * LS;  // this lane's block of every row
+    // CD key mask (|dec| bits above the index code), kept in a register so the
+    // per-coordinate key is a single LOP3 with the element code as immediate
+    // (index_base < 2^62: the OR adds nothing, but ptxas cannot fold it)
+    const unsigned kmask = (0x7FFFFFFFu & ~((1u << ((E * L <= 128) ? 7 : 8)) - 1u)) |
+                           (unsigned)(a.index_base >> 62);
 
-    float y[E], gr[E], qd[E];
+    // register arrays padded to an even length (packed FP32x2 math); the
+    // padding coordinates (k >= R) stay exactly zero
+    float y[EE], gr[EE], qd[EE];
 
     int status = ST_DONE;
     bool fail = false, write_x = false;
@@ -135,7 +170,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     // The problem's full linear term h (sum of the split-K partials, loads
     // issued 4 at a time) is staged once in shared memory: the short-circuit
     // scan and the compact gather h[act_idx[k]] both read it from there.
-    float *hrow = smem_f + R * S + (size_t)slot * r;
+    float *hrow = smem_f + R * SP + (size_t)slot * r;
     bool any_neg = false, frozen_neg = false;
     if (valid) {
         for (int i = l; i < r; i += L) {
@@ -159,7 +194,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     }
     const bool solve = valid && any_neg && !frozen_neg;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < EE; ++e) {
         const int k = e * L + l;
         float qv = 0.f, yv = 0.f;
         if (solve && k < ra) {
@@ -172,7 +207,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         gr[e] = qv;
     }
     if (solve) {
-        q_times<E, L>(gr, y, Qrow, S, gmask);
+        q_times_f<E, L, EE, EP>(gr, [&](int e) { return y[e]; }, Qsl, gmask);
         float n0 = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e)
@@ -202,8 +237,9 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
             nsq = gsum<L>(nsq, gmask);
             if (nsq > 0.f) {
 #pragma unroll
-                for (int e = 0; e < E; ++e) qd[e] = 0.f;
-                q_times_f<E, L>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qrow, S, gmask);
+                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                q_times_f<E, L, EE, EP>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qsl,
+                                        gmask);
                 float curv = 0.f;
 #pragma unroll
                 for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
@@ -222,8 +258,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                             return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
                         };
 #pragma unroll
-                        for (int e = 0; e < E; ++e) qd[e] = 0.f;
-                        q_times_f<E, L>(qd, delta, Qrow, S, gmask);
+                        for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                        q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask);
                         if (pass == 1) break;
                         float df = 0.f;
 #pragma unroll
@@ -257,54 +293,94 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                     }
                 }
             }
+            // Greedy CD (kernels.py:106-132).  The argmax is an integer max
+            // over packed keys: |dec| with its low IB bits replaced by an
+            // index code, (EMAX - e) << LB | (L - 1 - l), so equal truncated
+            // decreases resolve to the lowest coordinate k = e*L + l (strict >,
+            // kernels.py:119).  The lane part is OR-ed in after the in-lane
+            // 3-way tree, so the per-coordinate key is one LOP3 (mask in a
+            // register, element code an immediate).
             constexpr int IB = (R <= 128) ? 7 : 8;
             constexpr unsigned IMASK = (1u << IB) - 1u;
+            constexpr int LB = (L == 1) ? 0 : (L == 2) ? 1 : (L == 4) ? 2 : (L == 8) ? 3
+                             : (L == 16) ? 4 : 5;
+            constexpr int EB = IB - LB;
+            constexpr unsigned EMAXC = (1u << EB) - 1u;
+            static_assert(EE <= (1 << EB), "index code does not fit the key");
+            const unsigned lcode = (unsigned)(L - 1 - l);
             int pp = -1;
             float pdx = 0.f;
             for (int s = 0; s < ra; ++s) {
-                unsigned key[E];
+                if (s > 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
+                unsigned key[EE];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int k = e * L + l;
-                    float gi = gr[e];
-                    if (pp >= 0) {
-                        gi = fmaf(Qrow[e * L * S + pp], pdx, gi);
-                        gr[e] = gi;
-                    }
-                    const float dxi = -fminf(gi, y[e]);
-                    const float dec = dxi * fmaf(0.5f, dxi, gi);
-                    key[e] = (__float_as_uint(dec) & (0x7FFFFFFFu & ~IMASK)) | (IMASK - (unsigned)k);
+                for (int e = 0; e < EE; e += 2) {
+                    const float d0 = -fminf(gr[e], y[e]), d1 = -fminf(gr[e + 1], y[e + 1]);
+                    const float2 t = __ffma2_rn(make_float2(0.5f, 0.5f), make_float2(d0, d1),
+                                                make_float2(gr[e], gr[e + 1]));
+                    const float2 dc = __fmul2_rn(make_float2(d0, d1), t);
+                    key[e] = (__float_as_uint(dc.x) & kmask) | ((EMAXC - (unsigned)e) << LB);
+                    key[e + 1] = (__float_as_uint(dc.y) & kmask) |
+                                 ((EMAXC - (unsigned)(e + 1)) << LB);
                 }
 #pragma unroll
-                for (int w = 1; w < E; w <<= 1)
+                for (int w = 1; w < EE; w *= 3)
 #pragma unroll
-                    for (int e = 0; e + w < E; e += 2 * w) key[e] = max(key[e], key[e + w]);
-                unsigned kb = key[0];
+                    for (int e = 0; e < EE; e += 3 * w) {
+                        if (e + 2 * w < EE)
+                            key[e] = __vimax3_u32(key[e], key[e + w], key[e + 2 * w]);
+                        else if (e + w < EE)
+                            key[e] = max(key[e], key[e + w]);
+                    }
+                unsigned kb = key[0] | lcode;
 #pragma unroll
                 for (int o = L / 2; o > 0; o >>= 1) kb = max(kb, __shfl_xor_sync(gmask, kb, o, L));
                 if ((kb & ~IMASK) == 0u) {
                     pp = -1;
                     break;
                 }
-                const int p = (int)(IMASK - (kb & IMASK));
+                const int ep = (int)(EMAXC - ((kb & IMASK) >> LB));
+                const int lp = (int)((unsigned)(L - 1) - (kb & (unsigned)(L - 1)));
                 float dxo = 0.f;
+#ifndef NMFB_NNLS_OWNER_SWITCH
+#define NMFB_NNLS_OWNER_SWITCH 0
+#endif
+#if NMFB_NNLS_OWNER_SWITCH
+                if (l == lp) {
+                    // the owner lane updates its coordinate ep (a jump table
+                    // instead of a compare/select over all E registers)
+                    switch (ep) {
+#define NMFB_OWN(N)                                                      \
+    case N:                                                              \
+        if (N < E) {                                                     \
+            dxo = -fminf(gr[N < EE ? N : 0], y[N < EE ? N : 0]);         \
+            y[N < EE ? N : 0] += dxo;                                    \
+        }                                                                \
+        break;
+                        NMFB_OWN(0) NMFB_OWN(1) NMFB_OWN(2) NMFB_OWN(3) NMFB_OWN(4) NMFB_OWN(5)
+                        NMFB_OWN(6) NMFB_OWN(7) NMFB_OWN(8) NMFB_OWN(9) NMFB_OWN(10) NMFB_OWN(11)
+                        NMFB_OWN(12) NMFB_OWN(13) NMFB_OWN(14) NMFB_OWN(15) NMFB_OWN(16)
+                        NMFB_OWN(17) NMFB_OWN(18) NMFB_OWN(19) NMFB_OWN(20) NMFB_OWN(21)
+                        NMFB_OWN(22) NMFB_OWN(23) NMFB_OWN(24) NMFB_OWN(25) NMFB_OWN(26)
+                        NMFB_OWN(27) NMFB_OWN(28) NMFB_OWN(29) NMFB_OWN(30) NMFB_OWN(31)
+#undef NMFB_OWN
+                        default: break;
+                    }
+                }
+#else
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    if (e * L + l == p) {
+                    if (e == ep && l == lp) {
                         dxo = -fminf(gr[e], y[e]);
                         y[e] += dxo;
                     }
                 }
+#endif
                 moved = true;
-                pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, p % L, L);
-                pp = p;
+                pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, lp, L);
+                pp = ep * L + lp;
             }
-            if (pp >= 0) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    gr[e] = fmaf(Qrow[e * L * S + pp], pdx, gr[e]);
-                }
-            }
+            if (pp >= 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
             iters += 1;
             bool finite = true;
             float nk = 0.f;
@@ -396,9 +472,10 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
 template <typename TH, int E, int L, int B>
 static int launch_fast_variant(const NnlsLaunch &p) {
     auto a = make_args<float, TH>(p);
-    constexpr int R = E * L, S = R | 1;
-    // Q (R x S) + one staged h row (r floats) per problem slot
-    size_t smem = sizeof(float) * ((size_t)R * S + (size_t)32 * B * p.r);
+    constexpr int R = E * L, SP = L * nnls_ls(E);
+    // Q (R x SP, permuted rows) + one staged h row (r floats) per problem slot
+    size_t smem = sizeof(float) * ((size_t)R * SP + (size_t)32 * B * p.r);
+    if (smem > 227 * 1024) return NMFB_ERR_ARG;
     auto kern = nnls_fast_kernel<TH, E, L, B, false>;
     if (p.nmirror > 0) {
         if constexpr (std::is_same<TH, float>::value)
