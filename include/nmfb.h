@@ -313,6 +313,47 @@ int nmfb_data_stats(const void *a, int a_dtype, int64_t len, double *out, void *
 int nmfb_dot(const void *a, int a_dtype, const void *b, int b_dtype, int64_t len, double *out,
              void *workspace, void *stream);
 
+/* ---------------- sparse ingest on the device ----------------------------
+ * SparseMatrix.from_triplets (matrix.py:104-125), transpose (matrix.py:149-154)
+ * and _validate + require_nonnegative (matrix.py:81-101,169-178) on device
+ * buffers.  Stream-ordered; scratch from the stream's memory pool.
+ * info (device, NMFB_INGEST_CODES int64): info[c] = lowest offending
+ * triplet / column / position of check c, INT64_MAX when the check passed. */
+#define NMFB_INGEST_TRIPLET_RANGE 0 /* "triplet index out of range" */
+#define NMFB_INGEST_INDPTR_SPAN 1   /* "column pointers must span [0, nnz]" */
+#define NMFB_INGEST_INDPTR_ORDER 2  /* "column pointers must be non-decreasing" */
+#define NMFB_INGEST_ROW_RANGE 3     /* "row index out of range" */
+#define NMFB_INGEST_ROW_ORDER 4     /* "row indices not strictly increasing in column j" */
+#define NMFB_INGEST_NONFINITE 5     /* "sparse values must be finite" */
+#define NMFB_INGEST_NONPOSITIVE 6   /* "stored sparse values must be > 0" */
+#define NMFB_INGEST_CODES 7
+
+/* CSC from `count` triplets (i, j int64, v fp64): stable order by (col, row),
+ * duplicates summed in input order when sum_duplicates (fp64, bit-identical
+ * to np.add.at), zeros dropped.  Outputs: indptr (cols+1 int64), rowidx /
+ * vals (capacity count; vals in vals_dtype), *nnz_out (device int64).
+ * Requires rows < 2^31, count < 2^32. */
+int nmfb_csc_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t *i,
+                           const int64_t *j, const double *v, int sum_duplicates,
+                           int64_t *indptr, int32_t *rowidx, void *vals, int vals_dtype,
+                           int64_t *nnz_out, int64_t *info, void *stream);
+
+/* CSR of a CSC matrix (= CSC of its transpose): rowptr (rows+1 int64),
+ * colidx ascending within each row, values permuted alongside. */
+int nmfb_csc_to_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
+                    const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *rowptr,
+                    int32_t *colidx, void *cvals, void *stream);
+
+/* CSC invariants + finite / strictly positive values -> info. */
+int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
+                      const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
+                      void *stream);
+
+/* int64 -> int32 index narrowing (info[NMFB_INGEST_ROW_RANGE] = first
+ * element that does not fit). */
+int nmfb_narrow_indices(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,6 +27,10 @@ F32, F64 = 0, 1
 MODE_FAST, MODE_REFERENCE = 0, 1
 FAIL_NONE = -1
 FASTBREAK_BLOCK = 32
+# sparse-ingest check codes (include/nmfb.h NMFB_INGEST_*)
+INGEST_TRIPLET_RANGE, INGEST_INDPTR_SPAN, INGEST_INDPTR_ORDER, INGEST_ROW_RANGE, \
+    INGEST_ROW_ORDER, INGEST_NONFINITE, INGEST_NONPOSITIVE = range(7)
+INGEST_CODES = 7
 UINT64_MAX = (1 << 64) - 1
 
 _vp = ctypes.c_void_p
@@ -94,6 +98,11 @@ SIGNATURES = {
     "nmfb_peer_put": (_int, [_vp, _i64, _vp, _i32, _i32, _vp, _vp, ctypes.c_uint64, _i32, _vp]),
     "nmfb_peer_wait": (_int, [_vp, _i32, ctypes.c_uint64, _f64, _vp]),
     "nmfb_sum_slots_f64": (_int, [_vp, _i32, _i64, _i64, _vp, _vp]),
+    "nmfb_csc_from_triplets": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _int,
+                                      _vp, _vp, _vp]),
+    "nmfb_csc_to_csr": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
+    "nmfb_csc_validate": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp]),
+    "nmfb_narrow_indices": (_int, [_vp, _i64, _vp, _vp, _vp]),
 }
 
 MAX_PEERS = 8  # NMFB_MAX_PEERS
@@ -151,7 +160,8 @@ KERNELS_PER_CALL = {
     "nmfb_sum_parts": 1, "nmfb_dense_residual_kmajor": 2, "nmfb_csr_yt_chunked": 2, "nmfb_tc_gemm": 1, "nmfb_split_transpose": 1, "nmfb_transpose": 1,
     "nmfb_slice_u8": 1, "nmfb_residual_i8": 2, "nmfb_gram_rescale": 2, "nmfb_data_stats": 2,
     "nmfb_tc_gemm_rows": 1, "nmfb_nnls_batch_peers": 1, "nmfb_peer_put": 1, "nmfb_peer_wait": 1,
-    "nmfb_sum_slots_f64": 1,
+    "nmfb_sum_slots_f64": 1, "nmfb_csc_from_triplets": 11, "nmfb_csc_to_csr": 8,
+    "nmfb_csc_validate": 2, "nmfb_narrow_indices": 2,
 }
 
 

@@ -8,6 +8,18 @@
 #include "nmfb_internal.h"
 
 namespace nmfb {
+int csc_from_triplets_launch(int64_t rows, int64_t cols, int64_t count, const int64_t *i,
+                             const int64_t *j, const double *v, int sum_dup, int64_t *indptr,
+                             int32_t *rowidx, void *vals, int vals_dtype, int64_t *nnz_out,
+                             int64_t *info, cudaStream_t st);
+int csc_to_csr_launch(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
+                      const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *rowptr,
+                      int32_t *colidx, void *cvals, cudaStream_t st);
+int csc_validate_launch(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
+                        const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
+                        cudaStream_t st);
+int narrow_indices_launch(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
+                          cudaStream_t st);
 size_t gram_workspace_bytes(int64_t rows, int r);
 int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, double *out, void *ws,
                 cudaStream_t st);
@@ -373,6 +385,34 @@ int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, flo
 
 int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream) {
     return check(transpose_launch(in, rows, cols, out, (cudaStream_t)stream));
+}
+
+int nmfb_csc_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t *i,
+                           const int64_t *j, const double *v, int sum_duplicates,
+                           int64_t *indptr, int32_t *rowidx, void *vals, int vals_dtype,
+                           int64_t *nnz_out, int64_t *info, void *stream) {
+    return check(csc_from_triplets_launch(rows, cols, count, i, j, v, sum_duplicates, indptr,
+                                          rowidx, vals, vals_dtype, nnz_out, info,
+                                          (cudaStream_t)stream));
+}
+
+int nmfb_csc_to_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
+                    const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *rowptr,
+                    int32_t *colidx, void *cvals, void *stream) {
+    return check(csc_to_csr_launch(rows, cols, nnz, indptr, rowidx, vals, vals_dtype, rowptr,
+                                   colidx, cvals, (cudaStream_t)stream));
+}
+
+int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
+                      const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
+                      void *stream) {
+    return check(csc_validate_launch(rows, cols, nnz, indptr, rowidx, vals, vals_dtype, info,
+                                     (cudaStream_t)stream));
+}
+
+int nmfb_narrow_indices(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
+                        void *stream) {
+    return check(narrow_indices_launch(in, n, out, info, (cudaStream_t)stream));
 }
 
 int nmfb_dot(const void *a, int a_dtype, const void *b, int b_dtype, int64_t len, double *out,

@@ -120,6 +120,21 @@ def shard_bounds(total, workers):
     return [shards[0][0]] + [hi for _, hi in shards]
 
 
+def device_sums(x):
+    """(sum|x|, sum x^2) in fp64 on the device (nmfb_dot's fixed-order reduction)."""
+    ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=torch.float64,
+                     device=x.device)
+    out = torch.zeros(3, dtype=torch.float64, device=x.device)
+    L.call("nmfb_dot", vp(x), _CODE["fp64" if x.dtype == torch.float64 else "fp32"], None,
+           L.F64, x.numel(), vp(out), vp(ws), stream_handle())
+    o = out.cpu().numpy()
+    return float(o[1]), float(o[2])
+
+
+def device_sum_squares(x):
+    return device_sums(x)[1]
+
+
 # ---------------------------------------------------------------------------
 # data matrix on the device
 # ---------------------------------------------------------------------------
@@ -145,25 +160,34 @@ class DeviceData:
             self.XT = V.t().contiguous().to(self.device, dt, non_blocking=True)
             self.host = None
             return
-        if isinstance(V, SparseMatrix):
+        from .ingest import DeviceCsc
+
+        if isinstance(V, (SparseMatrix, DeviceCsc)):
+            # CSC uploaded (or already resident), its CSR twin built on the
+            # device (csrc/ingest.cu) instead of the host's argsort
             self.kind = "sparse"
             self.n, self.m = V.rows, V.cols
             if V.nnz >= 2**31 or self.n >= 2**31 or self.m >= 2**31:
                 raise ValueError("sparse sizes must fit int32 indices")
-            rowptr, colidx, cvals = V.csr()
-            self.indptr = torch.from_numpy(V.indptr).to(self.device, non_blocking=True)
-            self.rowidx = torch.from_numpy(V.indices.astype(np.int32)).to(self.device)
-            self.vals = torch.from_numpy(V.values).to(self.device, dt)
-            self.rowptr = torch.from_numpy(rowptr).to(self.device)
-            self.colidx = torch.from_numpy(colidx.astype(np.int32)).to(self.device)
-            self.cvals = torch.from_numpy(cvals).to(self.device, dt)
-            chunks, heavy, nslots = csr_chunk_plan(rowptr)
+            if isinstance(V, SparseMatrix):
+                csc = DeviceCsc.from_host(V, dtype=dt, device=self.device, validate=True)
+                self.xsq = V.sum_squares()
+            else:
+                csc = V
+                if csc.dtype != dt:
+                    csc = DeviceCsc(csc.rows, csc.cols, csc.indptr, csc.rowidx,
+                                    csc.values.to(dt), validate=False)
+                self.xsq = device_sum_squares(V.values)
+            self.indptr, self.rowidx, self.vals = csc.indptr, csc.rowidx, csc.values
+            self.rowptr, self.colidx, self.cvals = csc.csr()
+            # the row-chunk plan of the load-balanced Y^T pass: O(n) on the host
+            chunks, heavy, nslots = csr_chunk_plan(self.rowptr.cpu().numpy())
             self.chunks = torch.from_numpy(chunks).to(self.device)
             self.heavy = torch.from_numpy(heavy).to(self.device)
             self.nchunks, self.nheavy, self.nslots = len(chunks), len(heavy), nslots
-            self.xsq = V.sum_squares()
             self.nnz = V.nnz
-            self.host = V
+            self.host = V if isinstance(V, SparseMatrix) else None
+            self.csc = csc
         else:
             arr = np.asarray(V)
             if arr.ndim != 2:

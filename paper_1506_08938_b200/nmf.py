@@ -21,6 +21,7 @@ import numpy as np
 import torch
 
 from . import device as D
+from .ingest import DeviceCsc
 from .exceptions import NumericalFailureError
 from .matrix import (DenseMatrix, SparseMatrix, frobenius_objective, require_nonnegative,
                      sparse_col_times_dense)
@@ -216,6 +217,15 @@ class FitSession:
             total = D.validate_and_sum(data)
             if init is None:
                 init = scale_draws_device(draws, total / (n * m), cfg, data.device)
+        elif data is None and isinstance(V, DeviceCsc):
+            # sparse data already on the GPU (ingest.DeviceCsc): checked and
+            # averaged there; the init draws are the same host PCG64 stream
+            V.validate()
+            data = D.DeviceData(V, cfg.precision)
+            n, m = V.rows, V.cols
+            if init is None:
+                init = initial_factors_from_mean(n, m, D.device_sums(V.values)[0] / (n * m),
+                                                 cfg)
         elif data is None:
             V = _as_matrix(V)
             require_nonnegative(V, "data matrix")
