@@ -354,6 +354,18 @@ int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *in
 int nmfb_narrow_indices(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
                         void *stream);
 
+/* ---------------- multiplicative-update baseline (baselines.py:41-85) ----
+ * In place, per problem row x (count x r, dtype):
+ *   x_i <- x_i * (num_i / (sum_k Q[i][k] x_k + floor)),  num = -h,
+ * Q the raw fp64 Gram (r x r) and h in nmfb_nnls_batch's linear-term
+ * convention (h_parts partials summed and subtracted from h_base; pass
+ * h_base = 0 so num is the data product G^T V or V F^T).
+ * stats (nullable, device uint64): [0] += count (one update per subproblem,
+ * the reference's k_bar = 1 convention). */
+int nmfb_mur_update(int dtype, const double *Q, int32_t r, const void *h, int h_dtype,
+                    int32_t h_parts, int64_t h_ld, int64_t h_pstride, double h_base, void *x,
+                    int64_t count, double floor_, uint64_t *stats, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,9 @@
 #include "nmfb_internal.h"
 
 namespace nmfb {
+int mur_update_launch(int dtype, const double *Q, int r, const void *h, int h_dtype, int S,
+                      int64_t h_ld, int64_t h_pstride, double h_base, void *x, int64_t count,
+                      double floor_, uint64_t *stats, cudaStream_t st);
 int csc_from_triplets_launch(int64_t rows, int64_t cols, int64_t count, const int64_t *i,
                              const int64_t *j, const double *v, int sum_dup, int64_t *indptr,
                              int32_t *rowidx, void *vals, int vals_dtype, int64_t *nnz_out,
@@ -385,6 +388,13 @@ int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, flo
 
 int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream) {
     return check(transpose_launch(in, rows, cols, out, (cudaStream_t)stream));
+}
+
+int nmfb_mur_update(int dtype, const double *Q, int32_t r, const void *h, int h_dtype,
+                    int32_t h_parts, int64_t h_ld, int64_t h_pstride, double h_base, void *x,
+                    int64_t count, double floor_, uint64_t *stats, void *stream) {
+    return check(mur_update_launch(dtype, Q, r, h, h_dtype, h_parts, h_ld, h_pstride, h_base, x,
+                                   count, floor_, stats, (cudaStream_t)stream));
 }
 
 int nmfb_csc_from_triplets(int64_t rows, int64_t cols, int64_t count, const int64_t *i,

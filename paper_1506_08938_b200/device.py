@@ -33,6 +33,7 @@ from .exceptions import NumericalFailureError
 from .matrix import DenseMatrix, SparseMatrix
 
 _TORCH = {"fp32": torch.float32, "fp64": torch.float64}
+MUR_FLOOR = 1e-12  # baselines.py:20
 _CODE = {"fp32": L.F32, "fp64": L.F64}
 
 
@@ -230,9 +231,21 @@ class Alternation:
     """Device state of fit(): G (n, r), FT (m, r) and all step buffers."""
 
     def __init__(self, data: DeviceData, cfg, G0, FT0, max_iters, precision="fp32", lanes=0,
-                 kernel_mode=None, splits=None):
+                 kernel_mode=None, splits=None, solver="nnls"):
         self.d = data
         self.cfg = cfg
+        # solver "mur": the multiplicative-update baseline (baselines.py:41-85)
+        # on the same data products; it ignores the penalties in its steps
+        # (the logged objective keeps them, baselines.py:58-63)
+        if solver not in ("nnls", "mur"):
+            raise ValueError("solver must be 'nnls' or 'mur'")
+        self.solver = solver
+        if solver == "mur":
+            import dataclasses
+
+            self.step_cfg = dataclasses.replace(cfg, mu1=0.0, mu2=0.0, beta1=0.0, beta2=0.0)
+        else:
+            self.step_cfg = cfg
         self.prec = precision
         self.code = _CODE[precision]
         self.mode = (L.MODE_REFERENCE if precision == "fp64" else L.MODE_FAST) \
@@ -348,6 +361,11 @@ class Alternation:
                None, self._st())
 
     def nnls(self, side, h, h_dtype, parts, h_ld, pstride, h_base, x, count, stats):
+        if self.solver == "mur":
+            Q = self.Qg if side == 0 else self.Hf
+            L.call("nmfb_mur_update", self.code, vp(Q), self.r, vp(h), h_dtype, parts, h_ld,
+                   pstride, float(h_base), vp(x), count, MUR_FLOOR, vp(stats), self._st())
+            return
         # global index of problem 0: fast-break blocks are absolute (kernels.py:247)
         base = self.index_base_e if side == 0 else 0
         L.call("nmfb_nnls_batch", self.code, self.mode, vp(self.Qa[side]), vp(self.sa[side]),
@@ -364,7 +382,7 @@ class Alternation:
     def estep(self, k):
         """Coefficient step (parallel.run_estep): linear terms, NNLS over the
         m columns, then the accumulators H_f = F F^T and Y^T = X F^T."""
-        cfg, d, r = self.cfg, self.d, self.r
+        cfg, d, r = self.step_cfg, self.d, self.r
         n, m = self.n, self.m
         if not self.qg_valid:
             # Gram of G with the anti-lopsided rescale fused into its epilogue
@@ -444,7 +462,7 @@ class Alternation:
     def mstep(self, k):
         """Component step (parallel.run_mstep): NNLS over the n rows with
         h = beta1 - Y^T."""
-        cfg = self.cfg
+        cfg = self.step_cfg
         if not getattr(self, "hf_rescaled", False):
             self.rescale(self.Hf, 2.0 * cfg.beta2, 1)
         self.hf_rescaled = False

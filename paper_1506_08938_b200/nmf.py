@@ -203,7 +203,7 @@ class FitSession:
     device-resident loop separately from the end-to-end call.
     """
 
-    def __init__(self, V, cfg, on_iteration=None, init=None, data=None):
+    def __init__(self, V, cfg, on_iteration=None, init=None, data=None, solver="nnls"):
         self.cfg = cfg
         self.on_iteration = on_iteration
         if data is None and isinstance(V, torch.Tensor):
@@ -241,7 +241,7 @@ class FitSession:
         self.data = data
         G0, FT0 = init
         self.state = D.Alternation(data, cfg, G0, FT0, cfg.max_outer, precision=cfg.precision,
-                                   lanes=cfg.lanes)
+                                   lanes=cfg.lanes, solver=solver)
 
     def run(self):
         cfg, st = self.cfg, self.state

@@ -227,3 +227,132 @@ def solve(p: NqpProblem, stop: StopState | None = None, max_inner: int = DEFAULT
                        initial_passive_grad_norm_sq=norm0, final_passive_grad_norm_sq=norm_k,
                        passive_grad_norm_history=hh[:, 0].copy(),
                        objective_history=hh[:, 1].copy())
+
+
+@dataclass
+class NqpBatchSolution:
+    """Solutions of a batch of NQP problems sharing one Hessian (row k of each
+    array belongs to problem k; histories only when requested)."""
+
+    x: np.ndarray                     # (count, r)
+    grad: np.ndarray                  # (count, r) = H x + h
+    inner_iterations: np.ndarray      # (count,) int
+    initial_passive_grad_norm_sq: np.ndarray
+    final_passive_grad_norm_sq: np.ndarray
+    passive_grad_norm_history: np.ndarray | None = None  # (count, max_inner + 1), 0-padded
+    objective_history: np.ndarray | None = None
+
+    def __len__(self):
+        return self.x.shape[0]
+
+    def solution(self, k):
+        """Problem k as the single-problem NqpSolution that ``solve`` returns."""
+        it = int(self.inner_iterations[k])
+        nh = self.passive_grad_norm_history
+        oh = self.objective_history
+        return NqpSolution(
+            x=self.x[k].copy(), grad=self.grad[k].copy(), inner_iterations=it,
+            initial_passive_grad_norm_sq=float(self.initial_passive_grad_norm_sq[k]),
+            final_passive_grad_norm_sq=float(self.final_passive_grad_norm_sq[k]),
+            passive_grad_norm_history=None if nh is None else nh[k, : it + 1].copy(),
+            objective_history=None if oh is None else oh[k, : it + 1].copy())
+
+
+def solve_batch(H, h, x0=None, epsilon=DEFAULT_EPSILON, max_inner=DEFAULT_MAX_INNER,
+                max_stop=0.0, histories=True) -> NqpBatchSolution:
+    """``solve`` (nqp.py:217-320) for many problems sharing H: problem k is
+    NqpProblem(H, h[k], x0[k]) solved with its own StopState(epsilon,
+    max_stop).  One rescale of H and ONE kernel launch for the whole batch
+    (nmfb_nqp_solve, reference order, fp64); every problem's result is
+    bit-identical to ``solve`` on it alone.  The closed-form short-circuits
+    (h >= 0; a KKT warm start) are taken per problem as ``solve`` does.
+    Errors: DegenerateProblemError when every diagonal of H is frozen and a
+    problem needs the iterative solve; NumericalFailureError naming the
+    lowest failing problem (``index``) otherwise."""
+    import torch
+
+    from . import _lib as L
+    from . import device as D
+
+    H = np.asarray(H, dtype=np.float64)
+    h = np.atleast_2d(np.asarray(h, dtype=np.float64))
+    count, r = h.shape
+    NqpProblem(H, h[0] if count else np.zeros(H.shape[0]))  # H validation (nqp.py:52-61)
+    if x0 is None:
+        x0 = np.zeros((count, r))
+    x0 = np.atleast_2d(np.asarray(x0, dtype=np.float64))
+    if x0.shape != (count, r):
+        raise ValueError(f"x0 must be {count}x{r}")
+    if np.any(x0 < 0):
+        raise ValueError("x0 must be nonnegative")
+    StopState(epsilon, max_stop)  # argument validation
+    if max_inner < 1:
+        raise ValueError("max_inner must be >= 1")
+    grad0 = x0 @ H.T + h
+    pas = (x0 > 0) | (grad0 < 0)
+    norm0 = np.einsum("ij,ij->i", np.where(pas, grad0, 0.0), np.where(pas, grad0, 0.0))
+    # the KKT short-circuit is an exact-zero test: decide near-zero rows with
+    # the same matrix-vector product ``solve`` uses (nqp.py:241-253)
+    tiny = np.flatnonzero(norm0 <= 1e-20 * (1.0 + np.max(np.abs(grad0), axis=1)) ** 2)
+    for k in tiny:
+        grad0[k] = H @ x0[k] + h[k]
+        norm0[k] = _passive_norm_sq(x0[k], grad0[k])
+    zero_h = np.all(h >= 0.0, axis=1)
+    kkt = ~zero_h & (norm0 == 0.0)
+    run = np.flatnonzero(~zero_h & ~kkt)
+    x = np.where(zero_h[:, None], 0.0, x0)
+    iters = np.zeros(count, dtype=np.int64)
+    init = np.zeros(count)
+    final = np.zeros(count)
+    nh = np.zeros((count, max_inner + 1)) if histories else None
+    oh = np.zeros((count, max_inner + 1)) if histories else None
+    if histories:  # closed forms: a single history entry (nqp.py:233-253)
+        for k in np.flatnonzero(kkt):
+            oh[k, 0] = float(0.5 * x0[k] @ grad0[k] + 0.5 * h[k] @ x0[k])
+    if run.size:
+        scale, active, Qa, bufs = _device_rescale(H)
+        if not active.any():
+            raise DegenerateProblemError(
+                "all diagonal entries are numerically zero; objective is linear in every "
+                "variable")
+        bad = np.any(h[run][:, ~active] < 0.0, axis=1)
+        if bad.any():
+            k = int(run[np.flatnonzero(bad)[0]])
+            frozen = int(np.flatnonzero(~active & (h[k] < 0.0))[0])
+            raise NumericalFailureError(
+                f"objective is unbounded along degenerate dimension {frozen} "
+                f"(zero curvature, negative slope) in problem {k}", index=k,
+                last_x=x0[k].copy())
+        dev = bufs["Qa"].device
+        hd = torch.from_numpy(np.ascontiguousarray(h[run])).to(dev)
+        xd = torch.from_numpy(np.ascontiguousarray(x0[run])).to(dev)
+        it_d = torch.zeros((run.size,), dtype=torch.int32, device=dev)
+        fin_d = torch.zeros((run.size,), dtype=torch.float64, device=dev)
+        # without histories the kernel still records entry 0 (the initial
+        # rescaled passive-gradient norm that ``solve`` reports)
+        hl = max_inner + 1 if histories else 1
+        hist = torch.zeros((run.size, hl, 2), dtype=torch.float64, device=dev)
+        stats = torch.tensor([0, -1], dtype=torch.int64, device=dev)
+        L.call("nmfb_nqp_solve", D.vp(bufs["Qa"]), D.vp(bufs["sa"]), D.vp(bufs["act"]),
+               D.vp(bufs["active"]), r, D.vp(bufs["ra"]), D.vp(hd), D.vp(xd), int(run.size),
+               float(epsilon), int(max_inner), float(max_stop), D.vp(it_d), D.vp(fin_d),
+               D.vp(hist), hl, D.vp(stats), D.stream_handle())
+        it = it_d.cpu().numpy().astype(np.int64)
+        if np.any(it < 0):
+            k = int(run[np.flatnonzero(it < 0)[0]])
+            raise NumericalFailureError(
+                f"NaN/Inf after inner iterations (max {max_inner}) in problem {k}", index=k,
+                last_x=x0[k].copy())
+        x[run] = xd.cpu().numpy()
+        iters[run] = it
+        final[run] = fin_d.cpu().numpy()
+        hh = hist.cpu().numpy()
+        init[run] = hh[:, 0, 0]
+        if histories:
+            for t, k in enumerate(run):
+                nh[k, : it[t] + 1] = hh[t, : it[t] + 1, 0]
+                oh[k, : it[t] + 1] = hh[t, : it[t] + 1, 1]
+    return NqpBatchSolution(x=x, grad=x @ H.T + h, inner_iterations=iters,
+                            initial_passive_grad_norm_sq=init,
+                            final_passive_grad_norm_sq=final,
+                            passive_grad_norm_history=nh, objective_history=oh)
