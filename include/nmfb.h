@@ -366,6 +366,15 @@ int nmfb_mur_update(int dtype, const double *Q, int32_t r, const void *h, int h_
                     int32_t h_parts, int64_t h_ld, int64_t h_pstride, double h_base, void *x,
                     int64_t count, double floor_, uint64_t *stats, void *stream);
 
+/* ---------------- seeded initial factors (nmf.py:115-127) ---------------
+ * numpy default_rng(seed) PCG64 stream regenerated on the device, bit-identical
+ * to the host draw: G (n x r, row-major) = U * scale drawn first, then
+ * F (r x m, C-order) = U * scale written transposed into FT (m x r).
+ * (state, inc) = np.random.PCG64(seed).state (128-bit, split hi/lo). */
+int nmfb_init_factors(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      int64_t n, int64_t m, int32_t r, double scale, int dtype, void *G,
+                      void *FT, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

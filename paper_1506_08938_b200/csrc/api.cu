@@ -8,6 +8,9 @@
 #include "nmfb_internal.h"
 
 namespace nmfb {
+int pcg64_factors_launch(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                         int64_t n, int64_t m, int r, double scale, int dtype, void *G, void *FT,
+                         cudaStream_t st);
 int mur_update_launch(int dtype, const double *Q, int r, const void *h, int h_dtype, int S,
                       int64_t h_ld, int64_t h_pstride, double h_base, void *x, int64_t count,
                       double floor_, uint64_t *stats, cudaStream_t st);
@@ -388,6 +391,13 @@ int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, flo
 
 int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream) {
     return check(transpose_launch(in, rows, cols, out, (cudaStream_t)stream));
+}
+
+int nmfb_init_factors(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      int64_t n, int64_t m, int32_t r, double scale, int dtype, void *G,
+                      void *FT, void *stream) {
+    return check(pcg64_factors_launch(state_hi, state_lo, inc_hi, inc_lo, n, m, r, scale, dtype,
+                                      G, FT, (cudaStream_t)stream));
 }
 
 int nmfb_mur_update(int dtype, const double *Q, int32_t r, const void *h, int h_dtype,

@@ -69,12 +69,20 @@ __device__ __forceinline__ void axpy_row(float (&acc)[EE], const float *row, flo
 // acc[e] += sum_j Q[k_e, j] * src(j), src(j) owned by lane (j % L), element
 // j / L; the source values come from a functor of the element index (held or
 // recomputed: d = passive gradient, delta = step).
+//
+// The groups of a warp start the source-lane loop at different offsets
+// (rot, one per quarter-warp), so the four quarter-warp phases of a 16-byte
+// load fetch four different rows instead of the same row four times
+// (shared-memory bandwidth, not a broadcast, is what a quarter-warp phase
+// costs).  Each problem's summation order is fixed by its slot in the warp
+// (its index mod 32), so results do not depend on sharding.
 template <int E, int L, int EE, int EP, typename F>
 __device__ __forceinline__ void q_times_f(float (&acc)[EE], F src, const float *Qs_l,
-                                          unsigned gmask) {
+                                          unsigned gmask, int rot) {
     constexpr int SP = L * nnls_ls(E);
 #pragma unroll 1
-    for (int jl = 0; jl < L; ++jl) {
+    for (int t = 0; t < L; ++t) {
+        const int jl = (t + rot) & (L - 1);
 #pragma unroll
         for (int je = 0; je < E; ++je) {
             const float mine = src(je);
@@ -122,6 +130,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     __shared__ float blk_norm[B][32], blk_final[B][32];
     __shared__ int blk_status[B][32];
     __shared__ int blk_any[B];
+    __shared__ int act_s[R];      // act_idx / scale_a staged once per CTA
+    __shared__ float scl_s[R];
 
     const int tid = threadIdx.x;
     const int ra = a.ra_dev ? *a.ra_dev : a.ra, r = a.r;
@@ -130,10 +140,25 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         for (int idx = tid; idx < R * SP / 4; idx += blockDim.x)
             q4[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
-        // coalesced reads of the compact Q, scattered into the permuted rows
-        for (int row = tid >> 5; row < ra; row += blockDim.x >> 5)
-            for (int k = tid & 31; k < ra; k += 32)
-                Qs[row * SP + (k % L) * LS + k / L] = a.Qa[row * ra + k];
+        // coalesced reads of the compact Q (eight loads in flight per
+        // thread), scattered into the permuted rows
+        for (int row = tid >> 5; row < ra; row += blockDim.x >> 5) {
+            const float *src = a.Qa + (size_t)row * ra;
+            for (int k0 = tid & 31; k0 < ra; k0 += 256) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = (k0 + 32 * u < ra) ? src[k0 + 32 * u] : 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + 32 * u;
+                    if (k < ra) Qs[row * SP + (k % L) * LS + k / L] = v[u];
+                }
+            }
+        }
+        for (int k = tid; k < ra; k += blockDim.x) {
+            act_s[k] = a.act_idx[k];
+            scl_s[k] = a.scale_a[k];
+        }
     }
     __syncthreads();
 
@@ -151,6 +176,10 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     const bool valid = blk_live && (g >= a.index_base) && (j < a.count);
     const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
     const float *Qsl = Qs + l * LS;  // this lane's block of every row
+    // q_times source-lane rotation: one offset per quarter-warp (see q_times_f)
+    // (measured: pays at E = 25, costs at E <= 13, where the per-lane source
+    // lane and row offsets outweigh the saved shared-memory phases)
+    const int rot = (E < 20) ? 0 : (L >= 8) ? ((lane >> 3) * (L / 4)) & (L - 1) : (lane >> 3);
     // CD key mask (|dec| bits above the index code), kept in a register so the
     // per-coordinate key is a single LOP3 with the element code as immediate
     // (index_base < 2^62: the OR adds nothing, but ptxas cannot fold it)
@@ -198,8 +227,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         const int k = e * L + l;
         float qv = 0.f, yv = 0.f;
         if (solve && k < ra) {
-            const int ik = a.act_idx[k];
-            const float sv = a.scale_a[k];
+            const int ik = act_s[k];
+            const float sv = scl_s[k];
             qv = __fdiv_rn(hrow[ik], sv);
             yv = a.x[j * r + ik] * sv;
         }
@@ -207,7 +236,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         gr[e] = qv;
     }
     if (solve) {
-        q_times_f<E, L, EE, EP>(gr, [&](int e) { return y[e]; }, Qsl, gmask);
+        q_times_f<E, L, EE, EP>(gr, [&](int e) { return y[e]; }, Qsl, gmask, rot);
         float n0 = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e)
@@ -239,7 +268,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
 #pragma unroll
                 for (int e = 0; e < EE; ++e) qd[e] = 0.f;
                 q_times_f<E, L, EE, EP>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qsl,
-                                        gmask);
+                                        gmask, rot);
                 float curv = 0.f;
 #pragma unroll
                 for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
@@ -259,7 +288,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                         };
 #pragma unroll
                         for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-                        q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask);
+                        q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask, rot);
                         if (pass == 1) break;
                         float df = 0.f;
 #pragma unroll
@@ -445,7 +474,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int k = e * L + l;
-                if (k < ra) a.x[j * r + a.act_idx[k]] = __fdiv_rn(y[e], a.scale_a[k]);
+                if (k < ra) a.x[j * r + act_s[k]] = __fdiv_rn(y[e], scl_s[k]);
             }
         }
         if (MIRROR && (write_x || !any_neg)) {

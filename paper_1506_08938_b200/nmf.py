@@ -135,14 +135,24 @@ def scale_draws(draws, mean, cfg):
     return g, ft
 
 
-def scale_draws_device(draws, mean, cfg, device):
-    """scale_draws on the device (same fp64 products, so bit-identical factors;
-    the host only uploads the raw draws)."""
-    u_g, u_f = draws
+def device_initial_factors(n, m, mean, cfg, device=None):
+    """initial_factors on the GPU: numpy's PCG64 stream for cfg.seed
+    regenerated in parallel (csrc/init.cu), bit-identical to the host draw,
+    scaled by sqrt(mean / r) in fp64 and rounded once to cfg.precision's
+    dtype.  Returns device tensors (G (n, r), FT (m, r))."""
+    from . import _lib as L
+
+    device = device or D.require_cuda()
+    st = np.random.PCG64(cfg.seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    mask = (1 << 64) - 1
+    dt = torch.float32 if cfg.precision == "fp32" else torch.float64
+    G = torch.empty((n, cfg.rank), dtype=dt, device=device)
+    FT = torch.empty((m, cfg.rank), dtype=dt, device=device)
     scale = float(np.sqrt(mean / cfg.rank))
-    g = torch.from_numpy(u_g).to(device) * scale
-    ft = (torch.from_numpy(u_f).to(device) * scale).t().contiguous()
-    return g, ft
+    L.call("nmfb_init_factors", s >> 64, s & mask, inc >> 64, inc & mask, n, m, cfg.rank, scale,
+           L.F32 if dt == torch.float32 else L.F64, D.vp(G), D.vp(FT), D.stream_handle())
+    return G, FT
 
 
 def initial_factors_from_mean(n, m, mean, cfg):
@@ -211,12 +221,10 @@ class FitSession:
             # and take the mean for the init scale on the device
             data = D.DeviceData(V, cfg.precision)  # asynchronous upload
             n, m = data.n, data.m
-            # the init's uniform draws do not depend on the data: draw them on
-            # the host while the upload is in flight, scale once the mean is known
-            draws = initial_draws(n, m, cfg) if init is None else None
+            # the init is drawn on the device once the mean is known
             total = D.validate_and_sum(data)
             if init is None:
-                init = scale_draws_device(draws, total / (n * m), cfg, data.device)
+                init = device_initial_factors(n, m, total / (n * m), cfg, data.device)
         elif data is None and isinstance(V, DeviceCsc):
             # sparse data already on the GPU (ingest.DeviceCsc): checked and
             # averaged there; the init draws are the same host PCG64 stream
@@ -224,15 +232,17 @@ class FitSession:
             data = D.DeviceData(V, cfg.precision)
             n, m = V.rows, V.cols
             if init is None:
-                init = initial_factors_from_mean(n, m, D.device_sums(V.values)[0] / (n * m),
-                                                 cfg)
+                init = device_initial_factors(n, m, D.device_sums(V.values)[0] / (n * m), cfg,
+                                              data.device)
         elif data is None:
             V = _as_matrix(V)
             require_nonnegative(V, "data matrix")
             data = D.DeviceData(V, cfg.precision)
             n, m = _shape(V)
             if init is None:
-                init = initial_factors(V, cfg)
+                # the host mean (numpy's summation, as nmf.py:109-112), the
+                # draws on the device
+                init = device_initial_factors(n, m, _mean(V), cfg, data.device)
         else:
             n, m = data.n, data.m
             if init is None:

@@ -107,6 +107,7 @@ def run_mstep(Y, H_f, cfg, G):
     data.device, data.kind, data.n, data.m = dev, "none", n, 0
     st = D.Alternation.__new__(D.Alternation)
     st.d, st.cfg, st.prec, st.code = data, cfg, cfg.precision, D._CODE[cfg.precision]
+    st.step_cfg, st.solver = cfg, "nnls"
     st.mode = L.MODE_REFERENCE if cfg.precision == "fp64" else L.MODE_FAST
     st.lanes, st.n, st.m, st.r = cfg.lanes, n, 0, r
     st.G = torch.from_numpy(np.ascontiguousarray(G)).to(dev, dt)
