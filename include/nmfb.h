@@ -375,6 +375,27 @@ int nmfb_init_factors(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uin
                       int64_t n, int64_t m, int32_t r, double scale, int dtype, void *G,
                       void *FT, void *stream);
 
+/* ---------------- L2-blocked sparse data products (fp32, r % 4 == 0) -----
+ * The gathered factor's rows (G for G^T X, F^T for X F^T) are cut into nblk
+ * blocks of blk rows; pass b only walks the entries that gather from block b,
+ * so the block stays L2-resident.  seg ((outputs) x (nblk + 1) int64) holds
+ * each output's sub-range per block, built once per matrix by
+ * nmfb_csc_segments (CSC columns, row blocks) / nmfb_chunk_segments (CSR row
+ * chunks, column blocks).  Results are bit-identical to the unblocked
+ * kernels (the running sums are carried through the output in its own type).
+ * The linear term covers all m columns (h = mu1 - G^T X, h (m x r)). */
+int nmfb_csc_segments(const int64_t *indptr, const int32_t *rowidx, int64_t m, int64_t blk,
+                      int32_t nblk, int64_t *seg, void *stream);
+int nmfb_chunk_segments(const int64_t *chunks, int64_t nchunks, const int32_t *colidx,
+                        int64_t blk, int32_t nblk, int64_t *seg, void *stream);
+int nmfb_csc_linear_blocked(const int64_t *indptr, const int64_t *seg, int32_t nblk,
+                            const int32_t *rowidx, const float *vals, int64_t m, const float *G,
+                            int32_t r, double mu1, float *h, void *stream);
+int nmfb_csr_yt_chunked_blocked(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                                int64_t nheavy, const int64_t *seg, int32_t nblk,
+                                const int32_t *colidx, const float *vals, const float *FT,
+                                int32_t r, int yt_dtype, void *YT, void *part, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

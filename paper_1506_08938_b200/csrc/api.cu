@@ -8,6 +8,17 @@
 #include "nmfb_internal.h"
 
 namespace nmfb {
+int csc_segments_launch(const int64_t *indptr, const int32_t *rowidx, int64_t m, int64_t blk,
+                        int nblk, int64_t *seg, cudaStream_t st);
+int chunk_segments_launch(const int64_t *chunks, int64_t nchunks, const int32_t *colidx,
+                          int64_t blk, int nblk, int64_t *seg, cudaStream_t st);
+int csc_linear_vec_launch(const int64_t *indptr, const int64_t *seg, int nblk,
+                          const int32_t *rowidx, const float *vals, int64_t lo, int64_t hi,
+                          const float *G, int r, double mu1, float *h, cudaStream_t st);
+int csr_yt_chunked_vec_launch(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                              int64_t nheavy, const int64_t *seg, int nblk, const int32_t *colidx,
+                              const float *vals, const float *FT, int r, int yt_dtype, void *YT,
+                              void *part, cudaStream_t st);
 int pcg64_factors_launch(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                          int64_t n, int64_t m, int r, double scale, int dtype, void *G, void *FT,
                          cudaStream_t st);
@@ -391,6 +402,33 @@ int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, flo
 
 int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream) {
     return check(transpose_launch(in, rows, cols, out, (cudaStream_t)stream));
+}
+
+int nmfb_csc_segments(const int64_t *indptr, const int32_t *rowidx, int64_t m, int64_t blk,
+                      int32_t nblk, int64_t *seg, void *stream) {
+    return check(csc_segments_launch(indptr, rowidx, m, blk, nblk, seg, (cudaStream_t)stream));
+}
+
+int nmfb_chunk_segments(const int64_t *chunks, int64_t nchunks, const int32_t *colidx,
+                        int64_t blk, int32_t nblk, int64_t *seg, void *stream) {
+    return check(chunk_segments_launch(chunks, nchunks, colidx, blk, nblk, seg,
+                                       (cudaStream_t)stream));
+}
+
+int nmfb_csc_linear_blocked(const int64_t *indptr, const int64_t *seg, int32_t nblk,
+                            const int32_t *rowidx, const float *vals, int64_t m, const float *G,
+                            int32_t r, double mu1, float *h, void *stream) {
+    return check(csc_linear_vec_launch(indptr, seg, nblk, rowidx, vals, 0, m, G, r, mu1, h,
+                                       (cudaStream_t)stream));
+}
+
+int nmfb_csr_yt_chunked_blocked(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                                int64_t nheavy, const int64_t *seg, int32_t nblk,
+                                const int32_t *colidx, const float *vals, const float *FT,
+                                int32_t r, int yt_dtype, void *YT, void *part, void *stream) {
+    return check(csr_yt_chunked_vec_launch(chunks, nchunks, heavy, nheavy, seg, nblk, colidx,
+                                           vals, FT, r, yt_dtype, YT, part,
+                                           (cudaStream_t)stream));
 }
 
 int nmfb_init_factors(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,

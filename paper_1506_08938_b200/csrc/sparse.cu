@@ -213,6 +213,15 @@ __global__ void __launch_bounds__(128) csr_yt_chunk_v4_kernel(const int64_t *__r
     }
 }
 
+bool sparse_vec_ok(int r, const void *a, const void *b);
+int csc_linear_vec_launch(const int64_t *indptr, const int64_t *seg, int nblk,
+                          const int32_t *rowidx, const float *vals, int64_t lo, int64_t hi,
+                          const float *G, int r, double mu1, float *h, cudaStream_t st);
+int csr_yt_chunked_vec_launch(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
+                              int64_t nheavy, const int64_t *seg, int nblk, const int32_t *colidx,
+                              const float *vals, const float *FT, int r, int yt_dtype, void *YT,
+                              void *part, cudaStream_t st);
+
 static bool v4_ok(int r, const void *a) {
     return r % 4 == 0 && r <= 128 && ((uintptr_t)a % 16) == 0;
 }
@@ -225,11 +234,9 @@ static int csc_linear_dispatch(const int64_t *indptr, const int32_t *rowidx, con
     const T *v = (const T *)vals;
     const T *g = (const T *)G;
     T *o = (T *)h;
-    if (!EXACT && sizeof(T) == 4 && v4_ok(r, G) && v4_ok(r, h)) {
-        csc_linear_v4_kernel<<<grid, 128, 0, st>>>(indptr, rowidx, (const float *)vals, lo, hi,
-                                                   (const float *)G, r, (float)mu1, (float *)h);
-        return launch_status();
-    }
+    if (!EXACT && sizeof(T) == 4 && sparse_vec_ok(r, G, h))  // 16-byte gathers, r <= 256
+        return csc_linear_vec_launch(indptr, nullptr, 1, rowidx, (const float *)vals, lo, hi,
+                                     (const float *)G, r, mu1, (float *)h, st);
 #define NMFB_CSC(Cc) \
     csc_linear_kernel<T, EXACT, Cc><<<grid, 128, 0, st>>>(indptr, rowidx, v, lo, hi, g, r, (T)mu1, o)
     if (r <= 32)
@@ -384,15 +391,10 @@ static int csr_yt_chunked_dispatch(const int64_t *chunks, int64_t nchunks, const
     const T *v = (const T *)vals;
     const T *f = (const T *)FT;
     TY *o = (TY *)YT, *pp = (TY *)part;
-    if (sizeof(T) == 4 && v4_ok(r, FT)) {
-        csr_yt_chunk_v4_kernel<TY><<<grid, 128, 0, st>>>(chunks, nchunks, colidx,
-                                                         (const float *)vals, (const float *)FT, r,
-                                                         o, pp);
-        if (nheavy > 0)
-            csr_yt_fold_kernel<TY><<<(unsigned)((nheavy + 3) / 4), 128, 0, st>>>(heavy, nheavy, r,
-                                                                                 pp, o);
-        return launch_status();
-    }
+    if (sizeof(T) == 4 && sparse_vec_ok(r, FT, FT))  // 16-byte gathers, r <= 256
+        return csr_yt_chunked_vec_launch(chunks, nchunks, heavy, nheavy, nullptr, 1, colidx,
+                                         (const float *)vals, (const float *)FT, r,
+                                         sizeof(TY) == 8 ? NMFB_F64 : NMFB_F32, YT, part, st);
 #define NMFB_CSRC(Cc) \
     csr_yt_chunk_kernel<T, TY, Cc><<<grid, 128, 0, st>>>(chunks, nchunks, colidx, v, f, r, o, pp)
     if (r <= 32)

@@ -121,6 +121,13 @@ def shard_bounds(total, workers):
     return [shards[0][0]] + [hi for _, hi in shards]
 
 
+def _count_launches(k):
+    """Extra kernel launches of a multi-pass entry point (gpu_launches)."""
+    rec = L.Recorder.active
+    if rec is not None:
+        rec.launches += k
+
+
 def device_sums(x):
     """(sum|x|, sum x^2) in fp64 on the device (nmfb_dot's fixed-order reduction)."""
     ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=torch.float64,
@@ -189,6 +196,7 @@ class DeviceData:
             self.nnz = V.nnz
             self.host = V if isinstance(V, SparseMatrix) else None
             self.csc = csc
+            self.blocking = {}
         else:
             arr = np.asarray(V)
             if arr.ndim != 2:
@@ -202,6 +210,36 @@ class DeviceData:
                 xt = xt.astype(np.float64)
             self.XT = torch.from_numpy(xt).to(self.device)
             self.host = None
+
+    def spmm_blocking(self, r):
+        """L2 blocking plan of the sparse data products for rank r (fp32):
+        (nblk_g, seg_g, nblk_f, seg_f) -- the gathered factor (G, n x r, for
+        G^T X; F^T, m x r, for X F^T) is cut into blocks of at most
+        NMFB_SPMM_BLOCK_MB (default 48) MB; one block means no blocking."""
+        import os
+
+        if r in self.blocking:
+            return self.blocking[r]
+        mb = float(os.environ.get("NMFB_SPMM_BLOCK_MB", "48"))
+        plan = []
+        for rows, build in ((self.n, "csc"), (self.m, "chunk")):
+            nblk = max(1, int(np.ceil(rows * r * 4 / (mb * 2**20)))) if mb > 0 else 1
+            if nblk == 1:
+                plan += [1, None]
+                continue
+            blk = -(-rows // nblk)
+            if build == "csc":
+                seg = torch.empty((self.m, nblk + 1), dtype=torch.int64, device=self.device)
+                L.call("nmfb_csc_segments", vp(self.indptr), vp(self.rowidx), self.m, blk, nblk,
+                       vp(seg), stream_handle())
+            else:
+                seg = torch.empty((self.nchunks, nblk + 1), dtype=torch.int64,
+                                  device=self.device)
+                L.call("nmfb_chunk_segments", vp(self.chunks), self.nchunks, vp(self.colidx),
+                       blk, nblk, vp(seg), stream_handle())
+            plan += [nblk, seg]
+        self.blocking[r] = tuple(plan)
+        return self.blocking[r]
 
     def ensure_x_rowmajor(self):
         """X (n, m) row-major next to X^T: the K-major operand of the Y^T pass
@@ -342,6 +380,13 @@ class Alternation:
         s = min(s, max(1, K // 256))
         return int(s)
 
+    def _spmm_plan(self):
+        """Blocked sparse products apply to the fp32 production path with
+        16-byte-aligned rows (r % 4 == 0, r <= 256)."""
+        if (self.mode != L.MODE_FAST or self.prec != "fp32" or self.r % 4 or self.r > 256):
+            return (1, None, 1, None)
+        return self.d.spmm_blocking(self.r)
+
     # -- primitive launches ------------------------------------------------
     def _st(self):
         return stream_handle()
@@ -412,8 +457,14 @@ class Alternation:
                        cfg.mu1, vp(self.hbuf), self._st())
                 self.nnls(0, self.hbuf, self.code, 0, r, 0, 0.0, self.FT, m, st)
         else:
-            L.call("nmfb_csc_linear", self.code, self.mode, vp(d.indptr), vp(d.rowidx),
-                   vp(d.vals), 0, m, vp(self.G), r, cfg.mu1, vp(self.hbuf), self._st())
+            nbg, segg = self._spmm_plan()[:2]
+            if nbg > 1:
+                L.call("nmfb_csc_linear_blocked", vp(d.indptr), vp(segg), nbg, vp(d.rowidx),
+                       vp(d.vals), m, vp(self.G), r, cfg.mu1, vp(self.hbuf), self._st())
+                _count_launches(nbg - 1)
+            else:
+                L.call("nmfb_csc_linear", self.code, self.mode, vp(d.indptr), vp(d.rowidx),
+                       vp(d.vals), 0, m, vp(self.G), r, cfg.mu1, vp(self.hbuf), self._st())
             self.nnls(0, self.hbuf, self.code, 0, r, 0, 0.0, self.FT, m, st)
         # accumulators from the new coefficients
         ba, bp = L.bounds_array(self.bounds_e)
@@ -451,9 +502,16 @@ class Alternation:
                 if getattr(self, "ypart", None) is None:
                     self.ypart = torch.empty((max(d.nslots, 1) * r,), dtype=self.ybuf.dtype,
                                              device=self.ybuf.device)
-                L.call("nmfb_csr_yt_chunked", self.code, vp(d.chunks), d.nchunks, vp(d.heavy),
-                       d.nheavy, vp(d.colidx), vp(d.cvals), vp(self.FT), r, ycode,
-                       vp(self.ybuf), vp(self.ypart), self._st())
+                nbf, segf = self._spmm_plan()[2:]
+                if nbf > 1:
+                    L.call("nmfb_csr_yt_chunked_blocked", vp(d.chunks), d.nchunks, vp(d.heavy),
+                           d.nheavy, vp(segf), nbf, vp(d.colidx), vp(d.cvals), vp(self.FT), r,
+                           ycode, vp(self.ybuf), vp(self.ypart), self._st())
+                    _count_launches(nbf - 1)
+                else:
+                    L.call("nmfb_csr_yt_chunked", self.code, vp(d.chunks), d.nchunks,
+                           vp(d.heavy), d.nheavy, vp(d.colidx), vp(d.cvals), vp(self.FT), r,
+                           ycode, vp(self.ybuf), vp(self.ypart), self._st())
             else:
                 L.call("nmfb_csr_yt", self.code, self.mode, vp(d.rowptr), vp(d.colidx),
                        vp(d.cvals), n, vp(self.FT), r, ycode, bp, W, vp(self.ybuf), self._st())

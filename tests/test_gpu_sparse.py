@@ -75,3 +75,26 @@ def test_sparse_products_match_fp64(r):
     want_y = Xf @ FT.astype(np.float64)
     got_y = yt.cpu().numpy()
     assert np.max(np.abs(got_y - want_y) / (want_y + 1e-30)) < 1e-12
+
+
+@pytest.mark.parametrize("r", [100, 200, 52])
+def test_blocked_spmm_bit_identical(r, monkeypatch):
+    """L2-blocked G^T X / X F^T passes (csrc/sparse_blocked.cu): a fit with
+    the gathered factors cut into ~1 MB blocks equals the unblocked fit bit
+    for bit (running sums carried exactly through the outputs)."""
+    from oracle import generators
+    from paper_1506_08938_b200 import NmfConfig, SparseMatrix
+    from paper_1506_08938_b200.nmf import FitSession
+
+    x = generators.sparse_zipf(20000, 8000, 2e-3, 9)
+    V = SparseMatrix(x.rows, x.cols, x.indptr, x.indices, x.values, validate=False)
+    cfg = NmfConfig(rank=r, max_outer=3, seed=2, rel_change_tol=0.0, precision="fp32")
+    monkeypatch.setenv("NMFB_SPMM_BLOCK_MB", "0")
+    m0, l0 = FitSession(V, cfg).run()
+    monkeypatch.setenv("NMFB_SPMM_BLOCK_MB", "1")
+    s1 = FitSession(V, cfg)
+    assert s1.state._spmm_plan()[0] > 1 and s1.state._spmm_plan()[2] > 1
+    m1, l1 = s1.run()
+    assert np.array_equal(m0.G.array, m1.G.array)
+    assert np.array_equal(m0.F.array, m1.F.array)
+    assert l0.objective == l1.objective
