@@ -215,14 +215,19 @@ class DeviceData:
         """L2 blocking plan of the sparse data products for rank r (fp32):
         (nblk_g, seg_g, nblk_f, seg_f) -- the gathered factor (G, n x r, for
         G^T X; F^T, m x r, for X F^T) is cut into blocks of at most
-        NMFB_SPMM_BLOCK_MB (default 48) MB; one block means no blocking."""
+        NMFB_SPMM_BLOCK_MB (G; default 96) / NMFB_SPMM_BLOCK_MB_F (F^T;
+        default 0 = off) MB; one block means no blocking.  Measured at config
+        5 (G 800 MB, F^T 160 MB): G^T X 7.0 -> 5.9 ms with 96 MB blocks; the
+        X F^T pass gets slower blocked (its outputs, n x r = 800 MB, would be
+        re-read and re-written every pass), so it stays unblocked."""
         import os
 
         if r in self.blocking:
             return self.blocking[r]
-        mb = float(os.environ.get("NMFB_SPMM_BLOCK_MB", "48"))
         plan = []
-        for rows, build in ((self.n, "csc"), (self.m, "chunk")):
+        for rows, build, var, dflt in ((self.n, "csc", "NMFB_SPMM_BLOCK_MB", "96"),
+                                       (self.m, "chunk", "NMFB_SPMM_BLOCK_MB_F", "0")):
+            mb = float(os.environ.get(var, dflt))
             nblk = max(1, int(np.ceil(rows * r * 4 / (mb * 2**20)))) if mb > 0 else 1
             if nblk == 1:
                 plan += [1, None]

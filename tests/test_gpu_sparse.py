@@ -90,8 +90,10 @@ def test_blocked_spmm_bit_identical(r, monkeypatch):
     V = SparseMatrix(x.rows, x.cols, x.indptr, x.indices, x.values, validate=False)
     cfg = NmfConfig(rank=r, max_outer=3, seed=2, rel_change_tol=0.0, precision="fp32")
     monkeypatch.setenv("NMFB_SPMM_BLOCK_MB", "0")
+    monkeypatch.setenv("NMFB_SPMM_BLOCK_MB_F", "0")
     m0, l0 = FitSession(V, cfg).run()
     monkeypatch.setenv("NMFB_SPMM_BLOCK_MB", "1")
+    monkeypatch.setenv("NMFB_SPMM_BLOCK_MB_F", "1")
     s1 = FitSession(V, cfg)
     assert s1.state._spmm_plan()[0] > 1 and s1.state._spmm_plan()[2] > 1
     m1, l1 = s1.run()
