@@ -4,6 +4,12 @@
 
 #include "nnls_common.cuh"
 
+// smallest E (coordinates per lane, L = 8) that uses the warp-shared Q
+// product q_times_w4
+#ifndef NMFB_NNLS_W4_MIN_E
+#define NMFB_NNLS_W4_MIN_E 13
+#endif
+
 namespace nmfb {
 
 // ---------------------------------------------------------------------------
@@ -92,6 +98,89 @@ __device__ __forceinline__ void q_times_f(float (&acc)[EE], F src, const float *
     }
 }
 
+// Q * src for the 4 problems of a warp (L = 8) with every Q element loaded
+// ONCE per warp and used for all 4 problems: lane l computes rows
+// k = e4 * 32 + l of all four problems (accumulators a[e4][p]); the four
+// source values of column j are four shuffles.  Each Q load is a 32-bit load
+// of the permuted layout (bank-conflict-free for LS/4 odd), so a column costs
+// 4 shuffles + ceil(R/32) loads instead of E 16-byte loads per group --
+// 2.6x fewer shared-memory wavefronts at r = 200.  The accumulators move
+// between the group layout (lane l of group g: rows e*8 + l of problem g) and
+// the warp layout through `scr` (the warp's four h staging rows, free after
+// the prologue).  Per row, the j order is the same as q_times_f's, so the
+// result is bit-identical to it with rot = 0.
+template <int E, int EE, typename F>
+__device__ __forceinline__ void q_times_w4(float (&acc)[EE], F src, const float *Qs,
+                                           float *scr, int r, int lane) {
+    constexpr int L = 8, LS = nnls_ls(E), SP = L * LS;
+    constexpr int E4 = (E * L + 31) / 32;
+    const int l = lane & 7, g = lane >> 3;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int k = e * L + l;
+        if (k < r) scr[g * r + k] = acc[e];
+    }
+    __syncwarp();
+    float a[E4][4];
+#pragma unroll
+    for (int e4 = 0; e4 < E4; ++e4) {
+        const int k = e4 * 32 + lane;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) a[e4][p] = (k < r) ? scr[p * r + k] : 0.f;
+    }
+    __syncwarp();
+    const float *qcol = Qs + (lane & 7) * LS + (lane >> 3);  // + e4 * 4 + j * SP
+#pragma unroll 1
+    for (int jl = 0; jl < L; ++jl) {
+#pragma unroll
+        for (int je = 0; je < E; ++je) {
+            const float mine = src(je);
+            float sp[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) sp[p] = __shfl_sync(NMFB_FULL_MASK, mine, 8 * p + jl);
+            const float *row = qcol + (je * L + jl) * SP;
+#pragma unroll
+            for (int e4 = 0; e4 < E4; ++e4) {
+                const float q = row[e4 * 4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) a[e4][p] = fmaf(q, sp[p], a[e4][p]);
+            }
+        }
+    }
+#pragma unroll
+    for (int e4 = 0; e4 < E4; ++e4) {
+        const int k = e4 * 32 + lane;
+        if (k < r) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) scr[p * r + k] = a[e4][p];
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int k = e * L + l;
+        if (k < r) acc[e] = scr[g * r + k];
+    }
+    __syncwarp();
+}
+
+// Q * src for the problems with `cond`: the warp-shared product for L = 8 at
+// larger ranks (called from warp-uniform control flow; skipped only when no
+// problem of the warp needs it, zero sources for the others), else per group.
+template <int E, int L, int EE, int EP, typename F>
+__device__ __forceinline__ void qmul_if(bool cond, float (&acc)[EE], F src, const float *Qs,
+                                        const float *Qsl, float *wscr, int r, int lane,
+                                        unsigned gmask, int rot) {
+    if constexpr (L == 8 && E >= NMFB_NNLS_W4_MIN_E) {
+        if (__any_sync(NMFB_FULL_MASK, cond)) {
+            auto masked = [&](int e) { return cond ? src(e) : 0.f; };
+            q_times_w4<E, EE>(acc, masked, Qs, wscr, r, lane);
+        }
+    } else {
+        if (cond) q_times_f<E, L, EE, EP>(acc, src, Qsl, gmask, rot);
+    }
+}
+
 // h = h_base - sum of the split-K partials, with independent loads in flight
 // (four accumulators) instead of a load -> add dependency chain.
 template <typename TH>
@@ -176,6 +265,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     const bool valid = blk_live && (g >= a.index_base) && (j < a.count);
     const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
     const float *Qsl = Qs + l * LS;  // this lane's block of every row
+    // the warp's four h staging rows double as the q_times_w4 exchange buffer
+    float *wscr = smem_f + R * SP + (size_t)(warp * (32 / L)) * r;
     // q_times source-lane rotation: one offset per quarter-warp (see q_times_f)
     // (measured: pays at E = 25, costs at E <= 13, where the per-lane source
     // lane and row offsets outweigh the saved shared-memory phases)
@@ -235,8 +326,9 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         y[e] = yv;
         gr[e] = qv;
     }
+    qmul_if<E, L, EE, EP>(solve, gr, [&](int e) { return y[e]; }, Qs, Qsl, wscr, r, lane, gmask,
+                          rot);
     if (solve) {
-        q_times_f<E, L, EE, EP>(gr, [&](int e) { return y[e]; }, Qsl, gmask, rot);
         float n0 = 0.f;
 #pragma unroll
         for (int e = 0; e < E; ++e)
@@ -254,74 +346,166 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     // passive-set gradient component (kernels.py:59-64): g if y > 0 or g < 0
     auto pgrad = [](float yv, float gv) { return (yv > 0.f || gv < 0.f) ? gv : 0.f; };
     while (true) {
-        if (status == ST_RUNNING) {
-            bool moved = false;
+        const bool running = (status == ST_RUNNING);
+        bool moved = false;
+        if constexpr (L == 8 && E >= NMFB_NNLS_W4_MIN_E) {
+            // The Q products are issued from warp-uniform control flow (the
+            // warp-shared product needs every lane); problems that do not take a
+            // step contribute zero sources and keep their accumulators.
             // exact line search over the passive set (kernels.py:57-103)
             float nsq = 0.f;
+            if (running) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const float d = pgrad(y[e], gr[e]);
-                nsq = fmaf(d, d, nsq);
+                for (int e = 0; e < E; ++e) {
+                    const float d = pgrad(y[e], gr[e]);
+                    nsq = fmaf(d, d, nsq);
+                }
             }
             nsq = gsum<L>(nsq, gmask);
-            if (nsq > 0.f) {
+            const bool ls = running && nsq > 0.f;
 #pragma unroll
-                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-                q_times_f<E, L, EE, EP>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qsl,
-                                        gmask, rot);
+            for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+            qmul_if<E, L, EE, EP>(ls, qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qs, Qsl, wscr,
+                                  r, lane, gmask, rot);
+            float alpha = 1.f, step = 1.f;
+            bool clamped = false;
+            if (ls) {
                 float curv = 0.f;
 #pragma unroll
                 for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
                 curv = gsum<L>(curv, gmask);
-                const float alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
-                bool clamped = false;
+                alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
 #pragma unroll
                 for (int e = 0; e < E; ++e)
                     if (fmaf(-alpha, pgrad(y[e], gr[e]), y[e]) < 0.f) clamped = true;
                 clamped = gany<L>(clamped, gmask, gbase);
-                if (clamped) {
-                    // _take_step (kernels.py:153-175) with the breakpoint fallback
-                    float step = alpha;
-                    for (int pass = 0; pass < 2; ++pass) {
-                        auto delta = [&](int e) {
-                            return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
-                        };
+            }
+            // _take_step (kernels.py:153-175) with the breakpoint fallback: the
+            // projected step at alpha, and once more at the breakpoint alpha_bp
+            // when the first one increases the objective
+            step = alpha;
+            auto delta = [&](int e) {
+                return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
+            };
+            const bool ts0 = ls && clamped;
+            if (ts0) {
 #pragma unroll
-                        for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-                        q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask, rot);
-                        if (pass == 1) break;
-                        float df = 0.f;
+                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+            }
+            qmul_if<E, L, EE, EP>(ts0, qd, delta, Qs, Qsl, wscr, r, lane, gmask, rot);
+            bool ts1 = false;
+            if (ts0) {
+                float df = 0.f;
 #pragma unroll
-                        for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
-                        df = gsum<L>(df, gmask);
-                        if (!(df > 0.f)) break;
-                        float abp = INFINITY;
+                for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
+                df = gsum<L>(df, gmask);
+                if (df > 0.f) {
+                    float abp = INFINITY;
 #pragma unroll
-                        for (int e = 0; e < E; ++e) {
-                            const float d = pgrad(y[e], gr[e]);
-                            if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
-                        }
-                        abp = gmin<L>(abp, gmask);
-                        if (!(abp < alpha)) break;
+                    for (int e = 0; e < E; ++e) {
+                        const float d = pgrad(y[e], gr[e]);
+                        if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                    }
+                    abp = gmin<L>(abp, gmask);
+                    if (abp < alpha) {
                         step = abp;
-                    }
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
-                        if (v != y[e]) moved = true;
-                        y[e] = v;
-                        gr[e] += qd[e];
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
-                        if (v != y[e]) moved = true;
-                        y[e] = v;
-                        gr[e] = fmaf(-alpha, qd[e], gr[e]);
+                        ts1 = true;
                     }
                 }
             }
+            if (ts1) {
+#pragma unroll
+                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+            }
+            qmul_if<E, L, EE, EP>(ts1, qd, delta, Qs, Qsl, wscr, r, lane, gmask, rot);
+            if (ts0) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
+                    if (v != y[e]) moved = true;
+                    y[e] = v;
+                    gr[e] += qd[e];
+                }
+            } else if (ls) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
+                    if (v != y[e]) moved = true;
+                    y[e] = v;
+                    gr[e] = fmaf(-alpha, qd[e], gr[e]);
+                }
+            }
+        } else {
+            if (running) {
+                // exact line search over the passive set (kernels.py:57-103)
+                float nsq = 0.f;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const float d = pgrad(y[e], gr[e]);
+                    nsq = fmaf(d, d, nsq);
+                }
+                nsq = gsum<L>(nsq, gmask);
+                if (nsq > 0.f) {
+#pragma unroll
+                    for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                    q_times_f<E, L, EE, EP>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qsl,
+                                            gmask, rot);
+                    float curv = 0.f;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
+                    curv = gsum<L>(curv, gmask);
+                    const float alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
+                    bool clamped = false;
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+                        if (fmaf(-alpha, pgrad(y[e], gr[e]), y[e]) < 0.f) clamped = true;
+                    clamped = gany<L>(clamped, gmask, gbase);
+                    if (clamped) {
+                        // _take_step (kernels.py:153-175) with the breakpoint fallback
+                        float step = alpha;
+                        for (int pass = 0; pass < 2; ++pass) {
+                            auto delta = [&](int e) {
+                                return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
+                            };
+#pragma unroll
+                            for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                            q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask, rot);
+                            if (pass == 1) break;
+                            float df = 0.f;
+#pragma unroll
+                            for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
+                            df = gsum<L>(df, gmask);
+                            if (!(df > 0.f)) break;
+                            float abp = INFINITY;
+#pragma unroll
+                            for (int e = 0; e < E; ++e) {
+                                const float d = pgrad(y[e], gr[e]);
+                                if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                            }
+                            abp = gmin<L>(abp, gmask);
+                            if (!(abp < alpha)) break;
+                            step = abp;
+                        }
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
+                            if (v != y[e]) moved = true;
+                            y[e] = v;
+                            gr[e] += qd[e];
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
+                            if (v != y[e]) moved = true;
+                            y[e] = v;
+                            gr[e] = fmaf(-alpha, qd[e], gr[e]);
+                        }
+                    }
+                }
+        }
+        }
+        if (running) {
             // Greedy CD (kernels.py:106-132).  The argmax is an integer max
             // over packed keys: |dec| with its low IB bits replaced by an
             // index code, (EMAX - e) << LB | (L - 1 - l), so equal truncated
