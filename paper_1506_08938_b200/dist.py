@@ -418,18 +418,35 @@ class CudaEngine:
         self.st.pieces[k].copy_(pieces)
 
 
+def csc_column_block(X, lo, hi):
+    """Columns [lo, hi) of a host CSC matrix (SparseMatrix or the oracle's
+    Csc) as a SparseMatrix sharing the index/value arrays."""
+    from .matrix import SparseMatrix
+
+    p0, p1 = int(X.indptr[lo]), int(X.indptr[hi])
+    return SparseMatrix(X.rows, hi - lo, X.indptr[lo:hi + 1] - p0, X.indices[p0:p1],
+                        X.values[p0:p1], validate=False)
+
+
 class DistFit:
     """bench.py / users: column-sharded fit state on this rank's GPU."""
 
-    def __init__(self, X_block, cfg, init, group=None):
+    def __init__(self, X_block, cfg, init, group=None, m_total=None):
+        """X_block: this rank's columns -- dense (n, m_local) or a sparse
+        SparseMatrix / ingest.DeviceCsc column block; m_total: the global
+        column count (default m_local * world, equal blocks).  The blocks
+        must be the ShardPlan's 32-aligned column ranges."""
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
-        n, m_local = X_block.shape
-        m = m_local * world
+        if hasattr(X_block, "shape"):
+            n, m_local = X_block.shape
+        else:
+            n, m_local = X_block.rows, X_block.cols
+        m = m_local * world if m_total is None else int(m_total)
         self.plan = ShardPlan(n, m, world)
         clo, chi = self.plan.col_range(rank)
         if chi - clo != m_local:
-            raise ValueError("every rank must hold a 32-aligned equal column block")
+            raise ValueError("every rank must hold its 32-aligned column block of the shard plan")
         G0, FT0 = init
         self.engine = CudaEngine(X_block, cfg, G0, FT0, cfg.max_outer, m)
         self.peer = False

@@ -25,18 +25,33 @@ def main(out_path):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rng = np.random.default_rng(3)
-    n, m, r, K = 1000, 2048, 50, 6
-    X = (rng.exponential(size=(n, r)) @ rng.exponential(size=(r, m))
-         + np.abs(rng.normal(0, 0.05, size=(n, m)))).astype(np.float32)
+    K = 6
+    if os.environ.get("NMFB_CHECK_SPARSE") == "1":
+        # sparse column block through DistFit(m_total=...) (the config 3/5
+        # strong-scaling path of bench.py)
+        from oracle import generators
+        from paper_1506_08938_b200.matrix import SparseMatrix
+
+        x = generators.sparse_zipf(6000, 3000, 4e-3, 5)
+        n, m, r = x.rows, x.cols, 40
+        X = SparseMatrix(x.rows, x.cols, x.indptr, x.indices, x.values, validate=False)
+        mean = float(x.values.sum()) / (n * m)
+        block = PD.csc_column_block(x, *PD.ShardPlan(n, m, 1).col_range(0))
+    else:
+        n, m, r = 1000, 2048, 50
+        X = (rng.exponential(size=(n, r)) @ rng.exponential(size=(r, m))
+             + np.abs(rng.normal(0, 0.05, size=(n, m)))).astype(np.float32)
+        mean = float(X.astype(np.float64).mean())
+        block = X
     cfg = NmfConfig(rank=r, max_outer=K, seed=0, rel_change_tol=0.0, precision="fp32")
-    G0, FT0 = initial_factors_from_mean(n, m, float(X.astype(np.float64).mean()), cfg)
+    G0, FT0 = initial_factors_from_mean(n, m, mean, cfg)
 
     single = FitSession(X, cfg, init=(G0, FT0)).state
     for k in range(K):
         single.iterate(k)
     single.join()
 
-    sess = PD.DistFit(X, cfg, init=(G0, FT0))
+    sess = PD.DistFit(block, cfg, init=(G0, FT0), m_total=m)
     st = sess.state
     for k in range(K):
         st.iterate(k)

@@ -163,3 +163,22 @@ def test_shard_plan_alignment():
         assert p.cols[-1][1] == m and p.rows[-1][1] == n
         assert sum(hi - lo for lo, hi in p.cols) == m
         assert p.row_chunk >= max(hi - lo for lo, hi in p.rows)
+
+
+def test_csc_column_block_slices():
+    from oracle import generators
+    from paper_1506_08938_b200.dist import ShardPlan, csc_column_block
+
+    x = generators.sparse_zipf(300, 257, 0.05, 3)
+    dense = np.zeros((x.rows, x.cols))
+    col_of = np.repeat(np.arange(x.cols), np.diff(x.indptr))
+    dense[x.indices, col_of] = x.values
+    for world in (1, 2, 3, 8):
+        plan = ShardPlan(x.rows, x.cols, world)
+        parts = []
+        for g in range(world):
+            lo, hi = plan.col_range(g)
+            b = csc_column_block(x, lo, hi)
+            assert b.cols == hi - lo and b.indptr[0] == 0 and b.indptr[-1] == b.nnz
+            parts.append(b.to_dense().array)
+        assert np.array_equal(np.concatenate(parts, 1), dense)

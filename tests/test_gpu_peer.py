@@ -237,3 +237,11 @@ def test_dist_world1_peer_and_nccl_paths_equal_single_gpu(tmp_path):
     for res in (peer, nccl):
         assert res["G_equal"] and res["FT_equal"], res
         assert res["obj_equal"], res
+
+
+def test_dist_world1_sparse_block_equals_single_gpu(tmp_path):
+    """torchrun, one rank, sparse data through DistFit(m_total=...) with the
+    shard plan's CSC column block (bench.py's config 3/5 strong-scaling
+    path): bit-identical to the single-GPU fit."""
+    res = _torchrun({"NMFB_CHECK_SPARSE": "1", "NMFB_DIST_PEER": "0"}, tmp_path, "sparse")
+    assert res["G_equal"] and res["FT_equal"] and res["obj_equal"], res
