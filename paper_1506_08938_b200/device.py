@@ -688,7 +688,19 @@ class Alternation:
         return None
 
     def factors_host(self):
-        return (self.G.double().cpu().numpy(), self.FT.double().cpu().numpy())
+        """(G, FT) as host float64 arrays for the model: G comes back
+        column-major (the reference's DenseMatrix layout, matrix.py:20-59) --
+        transposed on the device, so the host does no reordering pass -- and
+        both through pinned staging buffers (full-rate D2H)."""
+        Gt = self.G.t().to(torch.float64).contiguous()   # (r, n) = G column-major
+        FT = self.FT.to(torch.float64).contiguous()
+        out = []
+        for t in (Gt, FT):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            out.append(h)
+        torch.cuda.current_stream().synchronize()
+        return out[0].numpy().T, out[1].numpy()
 
 
 # ---------------------------------------------------------------------------
