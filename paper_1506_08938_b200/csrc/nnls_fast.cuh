@@ -293,26 +293,12 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     float *hrow = smem_f + R * SP + (size_t)slot * r;
     bool any_neg = false, frozen_neg = false;
     if (valid) {
-        // all of a lane's loads first (E independent partial-sum chains in
-        // flight), then the stores: hrow could alias the partials as far as
-        // the compiler knows, which would serialise load/store pairs
-        for (int i0 = 0; i0 < r; i0 += E * L) {
-            float hv[E];
-#pragma unroll
-            for (int t = 0; t < E; ++t) {
-                const int i = i0 + t * L + l;
-                hv[t] = (i < r) ? fast_h<TH>(a, j, i) : 0.f;
-            }
-#pragma unroll
-            for (int t = 0; t < E; ++t) {
-                const int i = i0 + t * L + l;
-                if (i < r) {
-                    hrow[i] = hv[t];
-                    if (hv[t] < 0.f) {
-                        any_neg = true;
-                        if (!a.active[i]) frozen_neg = true;
-                    }
-                }
+        for (int i = l; i < r; i += L) {
+            const float hv = fast_h<TH>(a, j, i);
+            hrow[i] = hv;
+            if (hv < 0.f) {
+                any_neg = true;
+                if (!a.active[i]) frozen_neg = true;
             }
         }
     }
