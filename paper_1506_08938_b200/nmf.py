@@ -71,6 +71,10 @@ class NmfConfig:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         if self.rank > 256:
             raise ValueError("rank must be <= 256 on this build")
+        if self.precision == "fp32" and self.rank > 224:
+            # the fp32 NNLS kernel stages the compact Q in shared memory
+            # (224 x 224 fp32 is the largest that fits next to its h rows)
+            raise ValueError("rank must be <= 224 with precision='fp32' (use 'fp64' above)")
 
 
 @dataclass

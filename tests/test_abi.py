@@ -66,3 +66,16 @@ def test_product_does_not_import_oracle():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M)
+
+
+def test_config_rank_limits():
+    """The fp32 NNLS kernel stages Q (r x r fp32) in shared memory: r <= 224;
+    the fp64 check mode goes to 256."""
+    from paper_1506_08938_b200 import NmfConfig
+
+    NmfConfig(rank=224, precision="fp32")
+    NmfConfig(rank=256, precision="fp64")
+    with pytest.raises(ValueError, match="224"):
+        NmfConfig(rank=225, precision="fp32")
+    with pytest.raises(ValueError):
+        NmfConfig(rank=257, precision="fp64")
