@@ -226,9 +226,20 @@ __global__ void __launch_bounds__(RQ_THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             int gl = 0, prev_rb = -1;
+            // X tiles beyond the 2-stage ring prefetched into L2, pd tiles
+            // ahead (NMFB_RQ_PREFETCH, 0 = off)
+            const int pd = (dbg >> 8) & 0xFF;
             for (int64_t t = t0; t < t1; ++t) {
                 const int it = (int)(t - t0), sf_ = it % NF, sx = it % NX;
                 const int rb = (int)(t / sched.col_tiles), ct = (int)(t % sched.col_tiles);
+                if (pd > NX) {
+                    for (int q = (it == 0 ? NX : pd); q <= pd; ++q) {
+                        const int64_t tq = t + q;
+                        if (tq < t1)
+                            tma_prefetch_2d(&tmX, (int)(tq % sched.col_tiles) * RQ_BN,
+                                            (int)(tq / sched.col_tiles) * RQ_BM);
+                    }
+                }
                 if (rb != prev_rb) {
                     // previous row block's MMAs must be done with the G slices
                     mbar_wait(g_empty, ((uint32_t)gl & 1u) ^ 1u);
@@ -478,7 +489,9 @@ int residual_i8_launch(const float *X, int64_t n, int64_t m, const void *Gsl, co
     double *part = (double *)ws;
     const int ksteps = (r + 31) / 32;
     // NMFB_RQ_DEBUG: 1 = skip epilogue math, 2 = skip MMAs (tuning aid only)
-    static const int dbg = getenv("NMFB_RQ_DEBUG") ? atoi(getenv("NMFB_RQ_DEBUG")) : 0;
+    static const int dbg = (getenv("NMFB_RQ_DEBUG") ? atoi(getenv("NMFB_RQ_DEBUG")) : 0) |
+                           ((getenv("NMFB_RQ_PREFETCH") ? atoi(getenv("NMFB_RQ_PREFETCH")) : 0)
+                            & 0xFF) << 8;
     if (ksteps == 1)
         launch_rq<64, 4, 3, 1>(tg, tf, tx, sg, sf, n, m, s, part, dbg, st);
     else if (ksteps == 2)

@@ -725,11 +725,19 @@ __global__ void __launch_bounds__(TC3_THREADS, 1)
     }
     if (warp == 0) {
         // ---------------- TMA producer (converged warp, elected issue) ----------------
+        // X tiles further ahead than the smem ring are prefetched into L2
+        // (distance pd k-blocks; NMFB_TC_PREFETCH, 0 = off), so each TMA load
+        // of the ring finds its tile in L2 instead of paying HBM latency
+        const int pd = (dbg >> 8) & 0xFF;
         int i = 0;
         for_each_segment(sched, blockIdx.x, [&](int tile, int kb0, int nkb, int, bool) {
             for (int t = 0; t < nkb; ++t, ++i) {
                 const int sx = i % NX, sf = i % NF;
                 const int kc = (kb0 + t) * TC_BK;
+                if (pd > NX) {
+                    for (int q = (t == 0 ? NX : pd); q <= pd; ++q)
+                        if (t + q < nkb) tma_prefetch_2d_elect(&tmX, kc + q * TC_BK, tile * TC3_BM);
+                }
                 mbar_wait(&xempty[sx], ((uint32_t)(i / NX) & 1u) ^ 1u);
                 mbar_expect_tx_elect(&xfull[sx], x_bytes);
                 tma_load_2d_elect(&tmX, &xfull[sx], xr + (size_t)sx * x_bytes, kc, tile * TC3_BM);
@@ -1022,7 +1030,9 @@ static void launch_tc3(const CUtensorMap &tx, const CUtensorMap &tb, const CUten
                              (int)smem);
         attr = true;
     }
-    static const int dbg = getenv("NMFB_TC_DEBUG") ? atoi(getenv("NMFB_TC_DEBUG")) : 0;
+    static const int dbg = (getenv("NMFB_TC_DEBUG") ? atoi(getenv("NMFB_TC_DEBUG")) : 0) |
+                           ((getenv("NMFB_TC_PREFETCH") ? atoi(getenv("NMFB_TC_PREFETCH")) : 0)
+                            & 0xFF) << 8;
     tc_gemm3_kernel<<<s.G, TC3_THREADS, smem, st>>>(tx, tb, tbl, out, M, N, s, chunk_kb, dbg);
 }
 

@@ -151,6 +151,25 @@ __device__ __forceinline__ void tma_load_2d_elect(const CUtensorMap *map, uint64
         : "memory");
 }
 
+// TMA prefetch of a tile into L2 (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d_elect(const CUtensorMap *map, int c0, int c1) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n"
+        "}\n" ::"l"((uint64_t)map),
+        "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     (uint64_t)map),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // host: cuTensorMapEncodeTiled through the runtime's driver entry point
 // ---------------------------------------------------------------------------
