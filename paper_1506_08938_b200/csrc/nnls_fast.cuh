@@ -688,13 +688,32 @@ static int launch_fast_variant(const NnlsLaunch &p) {
     constexpr int R = E * L, SP = L * nnls_ls(E);
     // Q (R x SP, permuted rows) + one staged h row (r floats) per problem slot
     size_t smem = sizeof(float) * ((size_t)R * SP + (size_t)32 * B * p.r);
-    if (smem > 227 * 1024) return NMFB_ERR_ARG;
+
     auto kern = nnls_fast_kernel<TH, E, L, B, false>;
     if (p.nmirror > 0) {
         if constexpr (std::is_same<TH, float>::value)
             kern = nnls_fast_kernel<TH, E, L, B, true>;
         else
             return NMFB_ERR_ARG;  // the fused all-gather takes fp32 partials
+    }
+    {
+        // dynamic + static shared memory must fit the opt-in per-block limit
+        // (227 KB): larger variants are an argument error, not a launch
+        // failure (queried once per instantiation)
+        static size_t limit = 0;
+        if (limit == 0) {
+            cudaFuncAttributes fa;
+            int dev = 0, optin = 0;
+            if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess ||
+                cudaGetDevice(&dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
+                    cudaSuccess) {
+                launch_status();
+                return NMFB_ERR_CUDA;
+            }
+            limit = (size_t)optin - fa.sharedSizeBytes;
+        }
+        if (smem > limit) return NMFB_ERR_ARG;
     }
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
