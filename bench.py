@@ -370,6 +370,7 @@ def run_ours(args):
             "peak_source": peak_src, "algorithmic_bytes_per_launch": sp_bytes,
             "avg_launch_ms": sp_avg, "timed": "live CUDA events in the timed steps",
             "gather_bytes_per_launch": 4.0 * nnz * R,
+            "gather_achieved_GBps": (4.0 * nnz * R) / (sp_avg / 1e3) / 1e9 if sp_avg > 0 else 0.0,
             "note": "compulsory bytes; the factor-row gathers (gather_bytes) are served "
                     "by L2 when the factor fits (C3), by HBM when it does not (C5)"}
     if "nmfb_nnls_batch" in calls:
