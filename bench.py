@@ -503,36 +503,47 @@ def cpu_baseline(X, bounded=True, iters=1):
 
 
 def run_reference(args):
+    """The reference's CPU path (the oracle port: C kernels restating the
+    numba shard kernels + numpy/OpenBLAS, as many shard threads as host
+    cores) on this arm's config; one step = one outer iteration, the state
+    carried between steps.  Sparse configs use the port's threaded C nnz loop
+    for the objective's cross term (same formula, matrix.py:240-253) and, at
+    config 5 (~30 s per iteration), run at most 2 timed steps after no warm-up
+    so the run stays within minutes."""
     world, rank, _ = dist_env()
     if rank != 0:
         return None
-    X = make_block(0)
-    n, m = X.shape
+    cid = args.config
+    X = make_block(0, cid)
+    sparse = not isinstance(X, np.ndarray)
+    n, m = (X.rows, X.cols) if sparse else X.shape
     from oracle import nmf_oracle as orc
 
     cores = os.cpu_count() or 1
-    cfg = orc.Config(rank=RANK, max_outer=args.warmup + args.steps, seed=SEED,
-                     rel_change_tol=0.0, workers=cores)
-    orc.fit(X[:64, :64], orc.Config(rank=4, max_outer=1, seed=0))
-    # warmup + timed steps of the same workload; the objective's numpy
-    # residual is part of the reference step (nmf.py:193-194)
+    knobs = config_knobs(cid)
+    steps, warmup = args.steps, args.warmup
+    if cid == 5:
+        steps, warmup = min(steps, 2), 0
+    cfg = orc.Config(max_outer=1, rel_change_tol=0.0, workers=cores, **knobs)
+    orc.fit(np.ones((64, 64)), orc.Config(rank=4, max_outer=1, seed=0))  # load the C library
     G, FT = orc.initial_factors(X, cfg)
     times = []
-    for k in range(args.warmup + args.steps):
+    for k in range(warmup + steps):
         t = time.perf_counter()
-        G, FT, _, _, _, _ = orc.one_iteration(X, G, FT, cfg)
+        G, FT, _ = orc.fit(X, cfg, init=(G, FT), chunked_objective=sparse)
         times.append(time.perf_counter() - t)
-    dt = sum(times[args.warmup:])
-    value = (n + m) * args.steps / dt
+    dt = sum(times[warmup:])
+    value = (n + m) * steps / dt
     return {"impl": "reference", "metric": "column NNLS solves/sec (NMF outer iteration: "
             "E+M steps + objective)", "value": value, "unit": "solves/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+            "steps": steps, "warmup": warmup, "ms_per_step": dt / steps * 1e3,
+            "higher_is_better": True, "scaling": "strong" if sparse else "weak",
+            "vs_baseline": None, "dtype": "fp64",
             "data": "synthetic (same generator as our arm)",
-            "config": {"workload": WORKLOAD, "n": n, "m": m, "rank": RANK},
+            "config": {"workload": WORKLOADS[cid], "n": n, "m": m, "rank": knobs["rank"]},
             "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} outer iterations of C2 (after "
-                                       f"{args.warmup} warm-up), oracle port, {cores} threads"},
+                             "sample": f"{steps} outer iterations of C{cid} (after {warmup} "
+                                       f"warm-up), oracle port, {cores} threads"},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
