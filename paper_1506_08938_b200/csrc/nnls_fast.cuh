@@ -252,444 +252,443 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     __syncthreads();
 
     // persistent: each CTA walks groups of B fast-break blocks (Q, act_idx and
-    // scale staged once per CTA instead of once per group); the loop body is
-    // left at the function's indentation
+    // scale staged once per CTA instead of once per group)
     const int64_t nblk_all = (a.index_base + a.count - 1) / 32 - a.index_base / 32 + 1;
     const int64_t ncta = (nblk_all + B - 1) / B;
     // (E < 13 launches one CTA per group: a single pass, no loop)
     constexpr bool PERSIST = E >= 13;
     for (int64_t cta = blockIdx.x; PERSIST ? cta < ncta : cta == (int64_t)blockIdx.x;
          cta += gridDim.x) {
-    const int warp = tid >> 5, lane = tid & 31;
-    const int l = lane % L;
-    const int gbase = lane - l;
-    const unsigned gmask = (L == 32) ? NMFB_FULL_MASK : (((1u << L) - 1u) << gbase);
-    const int slot = warp * (32 / L) + lane / L;  // problem slot in CTA
-    const int b = slot >> 5, pos = slot & 31;
-    const int64_t blk0 = a.index_base / 32;
-    const int64_t blk = blk0 + cta * B + b;
-    const bool blk_live = (blk * 32 - a.index_base) < a.count;
-    const int64_t g = blk * 32 + pos;
-    const int64_t j = g - a.index_base;
-    const bool valid = blk_live && (g >= a.index_base) && (j < a.count);
-    const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
-    const float *Qsl = Qs + l * LS;  // this lane's block of every row
-    // the warp's four h staging rows double as the q_times_w4 exchange buffer
-    float *wscr = smem_f + R * SP + (size_t)(warp * (32 / L)) * r;
-    // q_times source-lane rotation: one offset per quarter-warp (see q_times_f)
-    // (measured: pays at E = 25, costs at E <= 13, where the per-lane source
-    // lane and row offsets outweigh the saved shared-memory phases)
-    const int rot = (E < 20) ? 0 : (L >= 8) ? ((lane >> 3) * (L / 4)) & (L - 1) : (lane >> 3);
-    // CD key mask (|dec| bits above the index code), kept in a register so the
-    // per-coordinate key is a single LOP3 with the element code as immediate
-    // (index_base < 2^62: the OR adds nothing, but ptxas cannot fold it)
-    const unsigned kmask = (0x7FFFFFFFu & ~((1u << ((E * L <= 128) ? 7 : 8)) - 1u)) |
-                           (unsigned)(a.index_base >> 62);
+        const int warp = tid >> 5, lane = tid & 31;
+        const int l = lane % L;
+        const int gbase = lane - l;
+        const unsigned gmask = (L == 32) ? NMFB_FULL_MASK : (((1u << L) - 1u) << gbase);
+        const int slot = warp * (32 / L) + lane / L;  // problem slot in CTA
+        const int b = slot >> 5, pos = slot & 31;
+        const int64_t blk0 = a.index_base / 32;
+        const int64_t blk = blk0 + cta * B + b;
+        const bool blk_live = (blk * 32 - a.index_base) < a.count;
+        const int64_t g = blk * 32 + pos;
+        const int64_t j = g - a.index_base;
+        const bool valid = blk_live && (g >= a.index_base) && (j < a.count);
+        const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
+        const float *Qsl = Qs + l * LS;  // this lane's block of every row
+        // the warp's four h staging rows double as the q_times_w4 exchange buffer
+        float *wscr = smem_f + R * SP + (size_t)(warp * (32 / L)) * r;
+        // q_times source-lane rotation: one offset per quarter-warp (see q_times_f)
+        // (measured: pays at E = 25, costs at E <= 13, where the per-lane source
+        // lane and row offsets outweigh the saved shared-memory phases)
+        const int rot = (E < 20) ? 0 : (L >= 8) ? ((lane >> 3) * (L / 4)) & (L - 1) : (lane >> 3);
+        // CD key mask (|dec| bits above the index code), kept in a register so the
+        // per-coordinate key is a single LOP3 with the element code as immediate
+        // (index_base < 2^62: the OR adds nothing, but ptxas cannot fold it)
+        const unsigned kmask = (0x7FFFFFFFu & ~((1u << ((E * L <= 128) ? 7 : 8)) - 1u)) |
+                               (unsigned)(a.index_base >> 62);
 
-    // register arrays padded to an even length (packed FP32x2 math); the
-    // padding coordinates (k >= R) stay exactly zero
-    float y[EE], gr[EE], qd[EE];
+        // register arrays padded to an even length (packed FP32x2 math); the
+        // padding coordinates (k >= R) stay exactly zero
+        float y[EE], gr[EE], qd[EE];
 
-    int status = ST_DONE;
-    bool fail = false, write_x = false;
-    int iters = 0;
-    float final_norm = 0.f, norm_k = 0.f, threshold = 0.f;
+        int status = ST_DONE;
+        bool fail = false, write_x = false;
+        int iters = 0;
+        float final_norm = 0.f, norm_k = 0.f, threshold = 0.f;
 
-    // ---- prologue: short-circuit, frozen check, compact load, gradient ----
-    // The problem's full linear term h (sum of the split-K partials, loads
-    // issued 4 at a time) is staged once in shared memory: the short-circuit
-    // scan and the compact gather h[act_idx[k]] both read it from there.
-    float *hrow = smem_f + R * SP + (size_t)slot * r;
-    bool any_neg = false, frozen_neg = false;
-    if (valid) {
-        for (int i = l; i < r; i += L) {
-            const float hv = fast_h<TH>(a, j, i);
-            hrow[i] = hv;
-            if (hv < 0.f) {
-                any_neg = true;
-                if (!a.active[i]) frozen_neg = true;
-            }
-        }
-    }
-    __syncwarp(gmask);
-    any_neg = gany<L>(any_neg, gmask, gbase);
-    frozen_neg = gany<L>(frozen_neg, gmask, gbase);
-    if (valid) {
-        if (!any_neg) {
-            for (int i = l; i < r; i += L) a.x[j * r + i] = 0.f;
-        } else if (frozen_neg) {
-            fail = true;
-        }
-    }
-    const bool solve = valid && any_neg && !frozen_neg;
-#pragma unroll
-    for (int e = 0; e < EE; ++e) {
-        const int k = e * L + l;
-        float qv = 0.f, yv = 0.f;
-        if (solve && k < ra) {
-            const int ik = act_s[k];
-            const float sv = scl_s[k];
-            qv = __fdiv_rn(hrow[ik], sv);
-            yv = a.x[j * r + ik] * sv;
-        }
-        y[e] = yv;
-        gr[e] = qv;
-    }
-    qmul_if<E, L, EE, EP>(solve, gr, [&](int e) { return y[e]; }, Qs, Qsl, wscr, r, lane, gmask,
-                          rot);
-    if (solve) {
-        float n0 = 0.f;
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-            if (y[e] > 0.f || gr[e] < 0.f) n0 = fmaf(gr[e], gr[e], n0);
-        n0 = gsum<L>(n0, gmask);
-        write_x = true;
-        final_norm = n0;
-        if (n0 > 0.f) {
-            threshold = a.eps * n0;
-            status = ST_RUNNING;
-        }
-    }
-
-    // ---- lockstep iterations with per-block fast-break resolution ----
-    // passive-set gradient component (kernels.py:59-64): g if y > 0 or g < 0
-    auto pgrad = [](float yv, float gv) { return (yv > 0.f || gv < 0.f) ? gv : 0.f; };
-    while (true) {
-        const bool running = (status == ST_RUNNING);
-        bool moved = false;
-        if constexpr (L == 8 && E >= NMFB_NNLS_W4_MIN_E) {
-            // The Q products are issued from warp-uniform control flow (the
-            // warp-shared product needs every lane); problems that do not take a
-            // step contribute zero sources and keep their accumulators.
-            // exact line search over the passive set (kernels.py:57-103)
-            float nsq = 0.f;
-            if (running) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const float d = pgrad(y[e], gr[e]);
-                    nsq = fmaf(d, d, nsq);
+        // ---- prologue: short-circuit, frozen check, compact load, gradient ----
+        // The problem's full linear term h (sum of the split-K partials, loads
+        // issued 4 at a time) is staged once in shared memory: the short-circuit
+        // scan and the compact gather h[act_idx[k]] both read it from there.
+        float *hrow = smem_f + R * SP + (size_t)slot * r;
+        bool any_neg = false, frozen_neg = false;
+        if (valid) {
+            for (int i = l; i < r; i += L) {
+                const float hv = fast_h<TH>(a, j, i);
+                hrow[i] = hv;
+                if (hv < 0.f) {
+                    any_neg = true;
+                    if (!a.active[i]) frozen_neg = true;
                 }
             }
-            nsq = gsum<L>(nsq, gmask);
-            const bool ls = running && nsq > 0.f;
-#pragma unroll
-            for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-            qmul_if<E, L, EE, EP>(ls, qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qs, Qsl, wscr,
-                                  r, lane, gmask, rot);
-            float alpha = 1.f, step = 1.f;
-            bool clamped = false;
-            if (ls) {
-                float curv = 0.f;
-#pragma unroll
-                for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
-                curv = gsum<L>(curv, gmask);
-                alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                    if (fmaf(-alpha, pgrad(y[e], gr[e]), y[e]) < 0.f) clamped = true;
-                clamped = gany<L>(clamped, gmask, gbase);
+        }
+        __syncwarp(gmask);
+        any_neg = gany<L>(any_neg, gmask, gbase);
+        frozen_neg = gany<L>(frozen_neg, gmask, gbase);
+        if (valid) {
+            if (!any_neg) {
+                for (int i = l; i < r; i += L) a.x[j * r + i] = 0.f;
+            } else if (frozen_neg) {
+                fail = true;
             }
-            // _take_step (kernels.py:153-175) with the breakpoint fallback: the
-            // projected step at alpha, and once more at the breakpoint alpha_bp
-            // when the first one increases the objective
-            step = alpha;
-            auto delta = [&](int e) {
-                return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
-            };
-            const bool ts0 = ls && clamped;
-            if (ts0) {
+        }
+        const bool solve = valid && any_neg && !frozen_neg;
 #pragma unroll
-                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+        for (int e = 0; e < EE; ++e) {
+            const int k = e * L + l;
+            float qv = 0.f, yv = 0.f;
+            if (solve && k < ra) {
+                const int ik = act_s[k];
+                const float sv = scl_s[k];
+                qv = __fdiv_rn(hrow[ik], sv);
+                yv = a.x[j * r + ik] * sv;
             }
-            qmul_if<E, L, EE, EP>(ts0, qd, delta, Qs, Qsl, wscr, r, lane, gmask, rot);
-            bool ts1 = false;
-            if (ts0) {
-                float df = 0.f;
+            y[e] = yv;
+            gr[e] = qv;
+        }
+        qmul_if<E, L, EE, EP>(solve, gr, [&](int e) { return y[e]; }, Qs, Qsl, wscr, r, lane, gmask,
+                              rot);
+        if (solve) {
+            float n0 = 0.f;
 #pragma unroll
-                for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
-                df = gsum<L>(df, gmask);
-                if (df > 0.f) {
-                    float abp = INFINITY;
+            for (int e = 0; e < E; ++e)
+                if (y[e] > 0.f || gr[e] < 0.f) n0 = fmaf(gr[e], gr[e], n0);
+            n0 = gsum<L>(n0, gmask);
+            write_x = true;
+            final_norm = n0;
+            if (n0 > 0.f) {
+                threshold = a.eps * n0;
+                status = ST_RUNNING;
+            }
+        }
+
+        // ---- lockstep iterations with per-block fast-break resolution ----
+        // passive-set gradient component (kernels.py:59-64): g if y > 0 or g < 0
+        auto pgrad = [](float yv, float gv) { return (yv > 0.f || gv < 0.f) ? gv : 0.f; };
+        while (true) {
+            const bool running = (status == ST_RUNNING);
+            bool moved = false;
+            if constexpr (L == 8 && E >= NMFB_NNLS_W4_MIN_E) {
+                // The Q products are issued from warp-uniform control flow (the
+                // warp-shared product needs every lane); problems that do not take a
+                // step contribute zero sources and keep their accumulators.
+                // exact line search over the passive set (kernels.py:57-103)
+                float nsq = 0.f;
+                if (running) {
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
                         const float d = pgrad(y[e], gr[e]);
-                        if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                        nsq = fmaf(d, d, nsq);
                     }
-                    abp = gmin<L>(abp, gmask);
-                    if (abp < alpha) {
-                        step = abp;
-                        ts1 = true;
-                    }
-                }
-            }
-            if (ts1) {
-#pragma unroll
-                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-            }
-            qmul_if<E, L, EE, EP>(ts1, qd, delta, Qs, Qsl, wscr, r, lane, gmask, rot);
-            if (ts0) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
-                    if (v != y[e]) moved = true;
-                    y[e] = v;
-                    gr[e] += qd[e];
-                }
-            } else if (ls) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
-                    if (v != y[e]) moved = true;
-                    y[e] = v;
-                    gr[e] = fmaf(-alpha, qd[e], gr[e]);
-                }
-            }
-        } else {
-            if (running) {
-                // exact line search over the passive set (kernels.py:57-103)
-                float nsq = 0.f;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const float d = pgrad(y[e], gr[e]);
-                    nsq = fmaf(d, d, nsq);
                 }
                 nsq = gsum<L>(nsq, gmask);
-                if (nsq > 0.f) {
+                const bool ls = running && nsq > 0.f;
 #pragma unroll
-                    for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-                    q_times_f<E, L, EE, EP>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qsl,
-                                            gmask, rot);
+                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                qmul_if<E, L, EE, EP>(ls, qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qs, Qsl, wscr,
+                                      r, lane, gmask, rot);
+                float alpha = 1.f, step = 1.f;
+                bool clamped = false;
+                if (ls) {
                     float curv = 0.f;
 #pragma unroll
                     for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
                     curv = gsum<L>(curv, gmask);
-                    const float alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
-                    bool clamped = false;
+                    alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
 #pragma unroll
                     for (int e = 0; e < E; ++e)
                         if (fmaf(-alpha, pgrad(y[e], gr[e]), y[e]) < 0.f) clamped = true;
                     clamped = gany<L>(clamped, gmask, gbase);
-                    if (clamped) {
-                        // _take_step (kernels.py:153-175) with the breakpoint fallback
-                        float step = alpha;
-                        for (int pass = 0; pass < 2; ++pass) {
-                            auto delta = [&](int e) {
-                                return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
-                            };
+                }
+                // _take_step (kernels.py:153-175) with the breakpoint fallback: the
+                // projected step at alpha, and once more at the breakpoint alpha_bp
+                // when the first one increases the objective
+                step = alpha;
+                auto delta = [&](int e) {
+                    return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
+                };
+                const bool ts0 = ls && clamped;
+                if (ts0) {
 #pragma unroll
-                            for (int e = 0; e < EE; ++e) qd[e] = 0.f;
-                            q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask, rot);
-                            if (pass == 1) break;
-                            float df = 0.f;
+                    for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                }
+                qmul_if<E, L, EE, EP>(ts0, qd, delta, Qs, Qsl, wscr, r, lane, gmask, rot);
+                bool ts1 = false;
+                if (ts0) {
+                    float df = 0.f;
 #pragma unroll
-                            for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
-                            df = gsum<L>(df, gmask);
-                            if (!(df > 0.f)) break;
-                            float abp = INFINITY;
+                    for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
+                    df = gsum<L>(df, gmask);
+                    if (df > 0.f) {
+                        float abp = INFINITY;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const float d = pgrad(y[e], gr[e]);
+                            if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                        }
+                        abp = gmin<L>(abp, gmask);
+                        if (abp < alpha) {
+                            step = abp;
+                            ts1 = true;
+                        }
+                    }
+                }
+                if (ts1) {
+#pragma unroll
+                    for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                }
+                qmul_if<E, L, EE, EP>(ts1, qd, delta, Qs, Qsl, wscr, r, lane, gmask, rot);
+                if (ts0) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
+                        if (v != y[e]) moved = true;
+                        y[e] = v;
+                        gr[e] += qd[e];
+                    }
+                } else if (ls) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
+                        if (v != y[e]) moved = true;
+                        y[e] = v;
+                        gr[e] = fmaf(-alpha, qd[e], gr[e]);
+                    }
+                }
+            } else {
+                if (running) {
+                    // exact line search over the passive set (kernels.py:57-103)
+                    float nsq = 0.f;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const float d = pgrad(y[e], gr[e]);
+                        nsq = fmaf(d, d, nsq);
+                    }
+                    nsq = gsum<L>(nsq, gmask);
+                    if (nsq > 0.f) {
+#pragma unroll
+                        for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                        q_times_f<E, L, EE, EP>(qd, [&](int e) { return pgrad(y[e], gr[e]); }, Qsl,
+                                                gmask, rot);
+                        float curv = 0.f;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) curv = fmaf(pgrad(y[e], gr[e]), qd[e], curv);
+                        curv = gsum<L>(curv, gmask);
+                        const float alpha = (curv > 0.f) ? __fdiv_rn(nsq, curv) : 1.f;
+                        bool clamped = false;
+#pragma unroll
+                        for (int e = 0; e < E; ++e)
+                            if (fmaf(-alpha, pgrad(y[e], gr[e]), y[e]) < 0.f) clamped = true;
+                        clamped = gany<L>(clamped, gmask, gbase);
+                        if (clamped) {
+                            // _take_step (kernels.py:153-175) with the breakpoint fallback
+                            float step = alpha;
+                            for (int pass = 0; pass < 2; ++pass) {
+                                auto delta = [&](int e) {
+                                    return fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f) - y[e];
+                                };
+#pragma unroll
+                                for (int e = 0; e < EE; ++e) qd[e] = 0.f;
+                                q_times_f<E, L, EE, EP>(qd, delta, Qsl, gmask, rot);
+                                if (pass == 1) break;
+                                float df = 0.f;
+#pragma unroll
+                                for (int e = 0; e < E; ++e) df += delta(e) * fmaf(0.5f, qd[e], gr[e]);
+                                df = gsum<L>(df, gmask);
+                                if (!(df > 0.f)) break;
+                                float abp = INFINITY;
+#pragma unroll
+                                for (int e = 0; e < E; ++e) {
+                                    const float d = pgrad(y[e], gr[e]);
+                                    if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                                }
+                                abp = gmin<L>(abp, gmask);
+                                if (!(abp < alpha)) break;
+                                step = abp;
+                            }
 #pragma unroll
                             for (int e = 0; e < E; ++e) {
-                                const float d = pgrad(y[e], gr[e]);
-                                if (d > 0.f && y[e] > 0.f) abp = fminf(abp, __fdiv_rn(y[e], d));
+                                const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
+                                if (v != y[e]) moved = true;
+                                y[e] = v;
+                                gr[e] += qd[e];
                             }
-                            abp = gmin<L>(abp, gmask);
-                            if (!(abp < alpha)) break;
-                            step = abp;
-                        }
+                        } else {
 #pragma unroll
-                        for (int e = 0; e < E; ++e) {
-                            const float v = fmaxf(fmaf(-step, pgrad(y[e], gr[e]), y[e]), 0.f);
-                            if (v != y[e]) moved = true;
-                            y[e] = v;
-                            gr[e] += qd[e];
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < E; ++e) {
-                            const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
-                            if (v != y[e]) moved = true;
-                            y[e] = v;
-                            gr[e] = fmaf(-alpha, qd[e], gr[e]);
+                            for (int e = 0; e < E; ++e) {
+                                const float v = fmaf(-alpha, pgrad(y[e], gr[e]), y[e]);
+                                if (v != y[e]) moved = true;
+                                y[e] = v;
+                                gr[e] = fmaf(-alpha, qd[e], gr[e]);
+                            }
                         }
                     }
-                }
-        }
-        }
-        if (running) {
-            // Greedy CD (kernels.py:106-132).  The argmax is an integer max
-            // over packed keys: |dec| with its low IB bits replaced by an
-            // index code, (EMAX - e) << LB | (L - 1 - l), so equal truncated
-            // decreases resolve to the lowest coordinate k = e*L + l (strict >,
-            // kernels.py:119).  The lane part is OR-ed in after the in-lane
-            // 3-way tree, so the per-coordinate key is one LOP3 (mask in a
-            // register, element code an immediate).
-            constexpr int IB = (R <= 128) ? 7 : 8;
-            constexpr unsigned IMASK = (1u << IB) - 1u;
-            constexpr int LB = (L == 1) ? 0 : (L == 2) ? 1 : (L == 4) ? 2 : (L == 8) ? 3
-                             : (L == 16) ? 4 : 5;
-            constexpr int EB = IB - LB;
-            constexpr unsigned EMAXC = (1u << EB) - 1u;
-            static_assert(EE <= (1 << EB), "index code does not fit the key");
-            const unsigned lcode = (unsigned)(L - 1 - l);
-            int pp = -1;
-            float pdx = 0.f;
-            for (int s = 0; s < ra; ++s) {
-                if (s > 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
-                unsigned key[EE];
+            }
+            }
+            if (running) {
+                // Greedy CD (kernels.py:106-132).  The argmax is an integer max
+                // over packed keys: |dec| with its low IB bits replaced by an
+                // index code, (EMAX - e) << LB | (L - 1 - l), so equal truncated
+                // decreases resolve to the lowest coordinate k = e*L + l (strict >,
+                // kernels.py:119).  The lane part is OR-ed in after the in-lane
+                // 3-way tree, so the per-coordinate key is one LOP3 (mask in a
+                // register, element code an immediate).
+                constexpr int IB = (R <= 128) ? 7 : 8;
+                constexpr unsigned IMASK = (1u << IB) - 1u;
+                constexpr int LB = (L == 1) ? 0 : (L == 2) ? 1 : (L == 4) ? 2 : (L == 8) ? 3
+                                 : (L == 16) ? 4 : 5;
+                constexpr int EB = IB - LB;
+                constexpr unsigned EMAXC = (1u << EB) - 1u;
+                static_assert(EE <= (1 << EB), "index code does not fit the key");
+                const unsigned lcode = (unsigned)(L - 1 - l);
+                int pp = -1;
+                float pdx = 0.f;
+                for (int s = 0; s < ra; ++s) {
+                    if (s > 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
+                    unsigned key[EE];
 #pragma unroll
-                for (int e = 0; e < EE; e += 2) {
-                    const float d0 = -fminf(gr[e], y[e]), d1 = -fminf(gr[e + 1], y[e + 1]);
-                    const float2 t = __ffma2_rn(make_float2(0.5f, 0.5f), make_float2(d0, d1),
-                                                make_float2(gr[e], gr[e + 1]));
-                    const float2 dc = __fmul2_rn(make_float2(d0, d1), t);
-                    key[e] = (__float_as_uint(dc.x) & kmask) | ((EMAXC - (unsigned)e) << LB);
-                    key[e + 1] = (__float_as_uint(dc.y) & kmask) |
-                                 ((EMAXC - (unsigned)(e + 1)) << LB);
-                }
-#pragma unroll
-                for (int w = 1; w < EE; w *= 3)
-#pragma unroll
-                    for (int e = 0; e < EE; e += 3 * w) {
-                        if (e + 2 * w < EE)
-                            key[e] = __vimax3_u32(key[e], key[e + w], key[e + 2 * w]);
-                        else if (e + w < EE)
-                            key[e] = max(key[e], key[e + w]);
+                    for (int e = 0; e < EE; e += 2) {
+                        const float d0 = -fminf(gr[e], y[e]), d1 = -fminf(gr[e + 1], y[e + 1]);
+                        const float2 t = __ffma2_rn(make_float2(0.5f, 0.5f), make_float2(d0, d1),
+                                                    make_float2(gr[e], gr[e + 1]));
+                        const float2 dc = __fmul2_rn(make_float2(d0, d1), t);
+                        key[e] = (__float_as_uint(dc.x) & kmask) | ((EMAXC - (unsigned)e) << LB);
+                        key[e + 1] = (__float_as_uint(dc.y) & kmask) |
+                                     ((EMAXC - (unsigned)(e + 1)) << LB);
                     }
-                unsigned kb = key[0] | lcode;
 #pragma unroll
-                for (int o = L / 2; o > 0; o >>= 1) kb = max(kb, __shfl_xor_sync(gmask, kb, o, L));
-                if ((kb & ~IMASK) == 0u) {
-                    pp = -1;
-                    break;
-                }
-                const int ep = (int)(EMAXC - ((kb & IMASK) >> LB));
-                const int lp = (int)((unsigned)(L - 1) - (kb & (unsigned)(L - 1)));
-                float dxo = 0.f;
+                    for (int w = 1; w < EE; w *= 3)
+#pragma unroll
+                        for (int e = 0; e < EE; e += 3 * w) {
+                            if (e + 2 * w < EE)
+                                key[e] = __vimax3_u32(key[e], key[e + w], key[e + 2 * w]);
+                            else if (e + w < EE)
+                                key[e] = max(key[e], key[e + w]);
+                        }
+                    unsigned kb = key[0] | lcode;
+#pragma unroll
+                    for (int o = L / 2; o > 0; o >>= 1) kb = max(kb, __shfl_xor_sync(gmask, kb, o, L));
+                    if ((kb & ~IMASK) == 0u) {
+                        pp = -1;
+                        break;
+                    }
+                    const int ep = (int)(EMAXC - ((kb & IMASK) >> LB));
+                    const int lp = (int)((unsigned)(L - 1) - (kb & (unsigned)(L - 1)));
+                    float dxo = 0.f;
 #ifndef NMFB_NNLS_OWNER_SWITCH
 #define NMFB_NNLS_OWNER_SWITCH 0
 #endif
 #if NMFB_NNLS_OWNER_SWITCH
-                if (l == lp) {
-                    // the owner lane updates its coordinate ep (a jump table
-                    // instead of a compare/select over all E registers)
-                    switch (ep) {
+                    if (l == lp) {
+                        // the owner lane updates its coordinate ep (a jump table
+                        // instead of a compare/select over all E registers)
+                        switch (ep) {
 #define NMFB_OWN(N)                                                      \
-    case N:                                                              \
-        if (N < E) {                                                     \
-            dxo = -fminf(gr[N < EE ? N : 0], y[N < EE ? N : 0]);         \
-            y[N < EE ? N : 0] += dxo;                                    \
-        }                                                                \
-        break;
-                        NMFB_OWN(0) NMFB_OWN(1) NMFB_OWN(2) NMFB_OWN(3) NMFB_OWN(4) NMFB_OWN(5)
-                        NMFB_OWN(6) NMFB_OWN(7) NMFB_OWN(8) NMFB_OWN(9) NMFB_OWN(10) NMFB_OWN(11)
-                        NMFB_OWN(12) NMFB_OWN(13) NMFB_OWN(14) NMFB_OWN(15) NMFB_OWN(16)
-                        NMFB_OWN(17) NMFB_OWN(18) NMFB_OWN(19) NMFB_OWN(20) NMFB_OWN(21)
-                        NMFB_OWN(22) NMFB_OWN(23) NMFB_OWN(24) NMFB_OWN(25) NMFB_OWN(26)
-                        NMFB_OWN(27) NMFB_OWN(28) NMFB_OWN(29) NMFB_OWN(30) NMFB_OWN(31)
+        case N:                                                              \
+            if (N < E) {                                                     \
+                dxo = -fminf(gr[N < EE ? N : 0], y[N < EE ? N : 0]);         \
+                y[N < EE ? N : 0] += dxo;                                    \
+            }                                                                \
+            break;
+                            NMFB_OWN(0) NMFB_OWN(1) NMFB_OWN(2) NMFB_OWN(3) NMFB_OWN(4) NMFB_OWN(5)
+                            NMFB_OWN(6) NMFB_OWN(7) NMFB_OWN(8) NMFB_OWN(9) NMFB_OWN(10) NMFB_OWN(11)
+                            NMFB_OWN(12) NMFB_OWN(13) NMFB_OWN(14) NMFB_OWN(15) NMFB_OWN(16)
+                            NMFB_OWN(17) NMFB_OWN(18) NMFB_OWN(19) NMFB_OWN(20) NMFB_OWN(21)
+                            NMFB_OWN(22) NMFB_OWN(23) NMFB_OWN(24) NMFB_OWN(25) NMFB_OWN(26)
+                            NMFB_OWN(27) NMFB_OWN(28) NMFB_OWN(29) NMFB_OWN(30) NMFB_OWN(31)
 #undef NMFB_OWN
-                        default: break;
+                            default: break;
+                        }
                     }
-                }
 #else
 #pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        if (e == ep && l == lp) {
+                            dxo = -fminf(gr[e], y[e]);
+                            y[e] += dxo;
+                        }
+                    }
+#endif
+                    moved = true;
+                    pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, lp, L);
+                    pp = ep * L + lp;
+                }
+                if (pp >= 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
+                iters += 1;
+                bool finite = true;
+                float nk = 0.f;
+#pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    if (e == ep && l == lp) {
-                        dxo = -fminf(gr[e], y[e]);
-                        y[e] += dxo;
+                    if (!(isfinite(y[e]) && isfinite(gr[e]))) finite = false;
+                    if (y[e] > 0.f || gr[e] < 0.f) nk = fmaf(gr[e], gr[e], nk);
+                }
+                finite = !gany<L>(!finite, gmask, gbase);
+                nk = gsum<L>(nk, gmask);
+                if (!finite) {
+                    fail = true;
+                    write_x = false;
+                    status = ST_DONE;
+                    final_norm = 0.f;
+                } else {
+                    norm_k = nk;
+                    moved = gany<L>(moved, gmask, gbase);
+                    if (nk <= threshold || !moved || iters >= a.max_inner) {
+                        status = ST_DONE;
+                        final_norm = nk;
+                    } else {
+                        status = ST_WAITING;
                     }
                 }
-#endif
-                moved = true;
-                pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, lp, L);
-                pp = ep * L + lp;
             }
-            if (pp >= 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
-            iters += 1;
-            bool finite = true;
-            float nk = 0.f;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                if (!(isfinite(y[e]) && isfinite(gr[e]))) finite = false;
-                if (y[e] > 0.f || gr[e] < 0.f) nk = fmaf(gr[e], gr[e], nk);
-            }
-            finite = !gany<L>(!finite, gmask, gbase);
-            nk = gsum<L>(nk, gmask);
-            if (!finite) {
-                fail = true;
-                write_x = false;
-                status = ST_DONE;
-                final_norm = 0.f;
+            // ---- resolve the fast-break block ----
+            if (L == 1) {
+                if (!__any_sync(NMFB_FULL_MASK, status != ST_DONE)) break;
+                resolve_block_warp<float>(status, norm_k, final_norm, m0);
             } else {
-                norm_k = nk;
-                moved = gany<L>(moved, gmask, gbase);
-                if (nk <= threshold || !moved || iters >= a.max_inner) {
-                    status = ST_DONE;
-                    final_norm = nk;
-                } else {
-                    status = ST_WAITING;
+                const int bar = 1 + b;
+                if (l == 0) {
+                    blk_status[b][pos] = status;
+                    blk_norm[b][pos] = norm_k;
+                    blk_final[b][pos] = final_norm;
+                }
+                asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * L) : "memory");
+                if (warp == b * L) {
+                    int st = blk_status[b][lane];
+                    float fn = blk_final[b][lane];
+                    resolve_block_warp<float>(st, blk_norm[b][lane], fn, m0);
+                    blk_status[b][lane] = st;
+                    blk_final[b][lane] = fn;
+                    bool any = __any_sync(NMFB_FULL_MASK, st != ST_DONE);
+                    if (lane == 0) blk_any[b] = any ? 1 : 0;
+                }
+                asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * L) : "memory");
+                status = blk_status[b][pos];
+                final_norm = blk_final[b][pos];
+                const bool any = blk_any[b] != 0;
+                asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * L) : "memory");
+                if (!any) break;
+            }
+        }
+
+        // ---- epilogue ----
+        if (valid) {
+            if (write_x) {
+                for (int i = l; i < r; i += L) a.x[j * r + i] = 0.f;
+                __syncwarp(gmask);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int k = e * L + l;
+                    if (k < ra) a.x[j * r + act_s[k]] = __fdiv_rn(y[e], scl_s[k]);
                 }
             }
-        }
-        // ---- resolve the fast-break block ----
-        if (L == 1) {
-            if (!__any_sync(NMFB_FULL_MASK, status != ST_DONE)) break;
-            resolve_block_warp<float>(status, norm_k, final_norm, m0);
-        } else {
-            const int bar = 1 + b;
+            if (MIRROR && (write_x || !any_neg)) {
+                // fused all-gather: the finished row (read back after the group's
+                // stores) goes to the same offset in every mirror (peer GPUs)
+                __syncwarp(gmask);
+                for (int i = l; i < r; i += L) {
+                    const float v = a.x[j * r + i];
+                    for (int q = 0; q < a.nmirror; ++q) a.mirror[q][j * r + i] = v;
+                }
+            }
             if (l == 0) {
-                blk_status[b][pos] = status;
-                blk_norm[b][pos] = norm_k;
-                blk_final[b][pos] = final_norm;
+                if (a.iters_out) a.iters_out[j] = fail ? -1 : iters;
+                if (a.final_out) a.final_out[j] = fail ? 0.f : final_norm;
+                if (fail) atomicMin((unsigned long long *)&a.stats[1], (unsigned long long)g);
             }
-            asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * L) : "memory");
-            if (warp == b * L) {
-                int st = blk_status[b][lane];
-                float fn = blk_final[b][lane];
-                resolve_block_warp<float>(st, blk_norm[b][lane], fn, m0);
-                blk_status[b][lane] = st;
-                blk_final[b][lane] = fn;
-                bool any = __any_sync(NMFB_FULL_MASK, st != ST_DONE);
-                if (lane == 0) blk_any[b] = any ? 1 : 0;
-            }
-            asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * L) : "memory");
-            status = blk_status[b][pos];
-            final_norm = blk_final[b][pos];
-            const bool any = blk_any[b] != 0;
-            asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * L) : "memory");
-            if (!any) break;
         }
-    }
-
-    // ---- epilogue ----
-    if (valid) {
-        if (write_x) {
-            for (int i = l; i < r; i += L) a.x[j * r + i] = 0.f;
-            __syncwarp(gmask);
+        unsigned long long it = (valid && !fail && l == 0) ? (unsigned long long)iters : 0ull;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int k = e * L + l;
-                if (k < ra) a.x[j * r + act_s[k]] = __fdiv_rn(y[e], scl_s[k]);
-            }
-        }
-        if (MIRROR && (write_x || !any_neg)) {
-            // fused all-gather: the finished row (read back after the group's
-            // stores) goes to the same offset in every mirror (peer GPUs)
-            __syncwarp(gmask);
-            for (int i = l; i < r; i += L) {
-                const float v = a.x[j * r + i];
-                for (int q = 0; q < a.nmirror; ++q) a.mirror[q][j * r + i] = v;
-            }
-        }
-        if (l == 0) {
-            if (a.iters_out) a.iters_out[j] = fail ? -1 : iters;
-            if (a.final_out) a.final_out[j] = fail ? 0.f : final_norm;
-            if (fail) atomicMin((unsigned long long *)&a.stats[1], (unsigned long long)g);
-        }
-    }
-    unsigned long long it = (valid && !fail && l == 0) ? (unsigned long long)iters : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) it += __shfl_xor_sync(NMFB_FULL_MASK, it, o);
-    if (lane == 0 && it) atomicAdd(&a.stats[0], it);
-    if (PERSIST) __syncthreads();  // staging rows and block state reused by the next group
+        for (int o = 16; o > 0; o >>= 1) it += __shfl_xor_sync(NMFB_FULL_MASK, it, o);
+        if (lane == 0 && it) atomicAdd(&a.stats[0], it);
+        if (PERSIST) __syncthreads();  // staging rows and block state reused by the next group
     }
 }
 
