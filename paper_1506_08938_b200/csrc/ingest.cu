@@ -192,7 +192,23 @@ __global__ void info_init_kernel(int64_t *info) {
 struct Pool {
     cudaStream_t st;
     std::vector<void *> ptrs;
-    explicit Pool(cudaStream_t s) : st(s) {}
+    explicit Pool(cudaStream_t s) : st(s) {
+        // keep freed scratch in the device's default pool instead of returning
+        // it to the driver at every synchronisation (the default threshold 0
+        // makes each ingest re-map its GBs of scratch: 10-400 ms host stalls)
+        static bool tuned = false;
+        if (!tuned) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess &&
+                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            cudaGetLastError();
+            tuned = true;
+        }
+    }
     template <typename T>
     T *get(size_t n) {
         void *p = nullptr;
