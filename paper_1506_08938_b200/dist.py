@@ -126,6 +126,17 @@ class PeerExchange:
         L.call("nmfb_peer_put", D.vp(src), nbytes, L.ptr_array(self.ptrs(name, byte_offset)),
                self.world, self.rank, None, None, 0, 0, D.stream_handle())
 
+    def put_barrier(self, src, name, byte_offset):
+        """put() + barrier() in one kernel: the copy to every peer, then (after
+        all of its CTAs) this rank's epoch flag on every peer; then the wait."""
+        self.epoch += 1
+        nbytes = src.numel() * src.element_size()
+        L.call("nmfb_peer_put", D.vp(src), nbytes, L.ptr_array(self.ptrs(name, byte_offset)),
+               self.world, self.rank, self.flag_ptrs, D.vp(self.ticket), self.epoch, 1,
+               D.stream_handle())
+        L.call("nmfb_peer_wait", self.ptrs("flags")[self.rank], self.world, self.epoch,
+               self.timeout_s, D.stream_handle())
+
     def barrier(self):
         """All writes this rank issued so far (kernels earlier on the stream)
         are visible on every peer, and every peer's on this rank."""
@@ -341,8 +352,7 @@ class CudaEngine:
         st.index_base_e = col_offset
         st.qg_valid = False  # G is replicated exactly: Gram + rescale locally
         st.estep(k)          # the X F^T epilogue stores into the owners' slots
-        px.put(st.Hf, "hf", px.rank * r * r * 8)
-        px.barrier()
+        px.put_barrier(st.Hf, "hf", px.rank * r * r * 8)
         L.call("nmfb_sum_slots_f64", D.vp(self.hf_slots), px.world, r * r, r * r, D.vp(st.Hf),
                D.stream_handle())
         st.rescale(st.Hf, 2.0 * self.cfg.beta2, 1)
