@@ -396,6 +396,13 @@ int nmfb_csr_yt_chunked_blocked(const int64_t *chunks, int64_t nchunks, const in
                                 const int32_t *colidx, const float *vals, const float *FT,
                                 int32_t r, int yt_dtype, void *YT, void *part, void *stream);
 
+/* Multi-GPU H_f: out H = sum over S per-source r x r slots (slot order,
+ * slot s at slots + s * stride), then nmfb_rescale(H, diag_add, ...) -- one
+ * launch (the peer-memory path's replacement for an allreduce + rescale). */
+int nmfb_sum_slots_rescale(int dtype, const double *slots, int32_t S, int64_t stride, double *H,
+                           int32_t r, double diag_add, void *Qa, void *scale_a,
+                           int32_t *act_idx, uint8_t *active, int32_t *ra_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,9 @@
 #include "nmfb_internal.h"
 
 namespace nmfb {
+int sum_slots_rescale_launch(int dtype, const double *slots, int S, int64_t stride, double *H,
+                             int r, double diag_add, void *Qa, void *scale_a, int32_t *act_idx,
+                             uint8_t *active, int32_t *ra_dev, cudaStream_t st);
 int csc_segments_launch(const int64_t *indptr, const int32_t *rowidx, int64_t m, int64_t blk,
                         int nblk, int64_t *seg, cudaStream_t st);
 int chunk_segments_launch(const int64_t *chunks, int64_t nchunks, const int32_t *colidx,
@@ -402,6 +405,13 @@ int nmfb_split_transpose(const float *B, int64_t K, int32_t r, float *Bt_hi, flo
 
 int nmfb_transpose(const float *in, int64_t rows, int64_t cols, float *out, void *stream) {
     return check(transpose_launch(in, rows, cols, out, (cudaStream_t)stream));
+}
+
+int nmfb_sum_slots_rescale(int dtype, const double *slots, int32_t S, int64_t stride, double *H,
+                           int32_t r, double diag_add, void *Qa, void *scale_a,
+                           int32_t *act_idx, uint8_t *active, int32_t *ra_dev, void *stream) {
+    return check(sum_slots_rescale_launch(dtype, slots, S, stride, H, r, diag_add, Qa, scale_a,
+                                          act_idx, active, ra_dev, (cudaStream_t)stream));
 }
 
 int nmfb_csc_segments(const int64_t *indptr, const int32_t *rowidx, int64_t m, int64_t blk,

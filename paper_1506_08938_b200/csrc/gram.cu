@@ -242,6 +242,22 @@ __global__ void __launch_bounds__(1024) rescale_kernel(const double *__restrict_
     rescale_body<T>(G, r, diag_add, Qa, scale_a, act_idx, active, ra_dev, full_scale, sh);
 }
 
+// The multi-GPU H_f: sum the per-source r x r slots in source order (as
+// sum_slots_f64) into H, then rescale it -- one single-CTA launch.
+template <typename T>
+__global__ void __launch_bounds__(1024) sum_slots_rescale_kernel(
+    const double *__restrict__ slots, int S, int64_t stride, double *H, int r, double diag_add,
+    T *Qa, T *scale_a, int32_t *act_idx, uint8_t *active, int32_t *ra_dev) {
+    extern __shared__ double sh[];
+    for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+        double acc = slots[i];
+        for (int s = 1; s < S; ++s) acc += slots[(int64_t)s * stride + i];
+        H[i] = acc;
+    }
+    __syncthreads();
+    rescale_body<T>(H, r, diag_add, Qa, scale_a, act_idx, active, ra_dev, nullptr, sh);
+}
+
 // Gram reduce with the rescale fused into its epilogue: the CTA that finishes
 // last (ticket) runs the rescale on the completed Gram -- one launch and no
 // host round trip between the Gram and the rescaled Q (north star (2)).
@@ -336,6 +352,28 @@ int rescale_launch(int dtype, const double *G, int r, double diag_add, void *Qa,
         rescale_kernel<float><<<1, 1024, smem, st>>>(G, r, diag_add, (float *)Qa,
                                                     (float *)scale_a, act_idx, active, ra_dev,
                                                     full_scale);
+    return launch_status();
+}
+
+int sum_slots_rescale_launch(int dtype, const double *slots, int S, int64_t stride, double *H,
+                             int r, double diag_add, void *Qa, void *scale_a, int32_t *act_idx,
+                             uint8_t *active, int32_t *ra_dev, cudaStream_t st) {
+    if (r <= 0 || r > 4096 || S < 1 || !slots || !H) return NMFB_ERR_ARG;
+    size_t smem = 2 * r * sizeof(double) + r * sizeof(int);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(sum_slots_rescale_kernel<double>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(sum_slots_rescale_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (dtype == NMFB_F64)
+        sum_slots_rescale_kernel<double><<<1, 1024, smem, st>>>(
+            slots, S, stride, H, r, diag_add, (double *)Qa, (double *)scale_a, act_idx, active,
+            ra_dev);
+    else
+        sum_slots_rescale_kernel<float><<<1, 1024, smem, st>>>(
+            slots, S, stride, H, r, diag_add, (float *)Qa, (float *)scale_a, act_idx, active,
+            ra_dev);
     return launch_status();
 }
 

@@ -353,9 +353,9 @@ class CudaEngine:
         st.qg_valid = False  # G is replicated exactly: Gram + rescale locally
         st.estep(k)          # the X F^T epilogue stores into the owners' slots
         px.put_barrier(st.Hf, "hf", px.rank * r * r * 8)
-        L.call("nmfb_sum_slots_f64", D.vp(self.hf_slots), px.world, r * r, r * r, D.vp(st.Hf),
-               D.stream_handle())
-        st.rescale(st.Hf, 2.0 * self.cfg.beta2, 1)
+        L.call("nmfb_sum_slots_rescale", st.code, D.vp(self.hf_slots), px.world, r * r,
+               D.vp(st.Hf), r, 2.0 * self.cfg.beta2, D.vp(st.Qa[1]), D.vp(st.sa[1]),
+               D.vp(st.act[1]), D.vp(st.active[1]), D.vp(st.ra[1]), D.stream_handle())
 
     def mstep_peer(self, k, lo, hi):
         st, px, r = self.st, self.px, self.r
