@@ -69,6 +69,126 @@ def test_host_mirror_errors_match_reference(name):
     assert type(ei.value).__name__ == typ and str(ei.value) == msg
 
 
+def test_host_validate_catches_each_invariant():
+    """The host constructor's checks on hand-broken CSC arrays, with the
+    reference's exception types and messages (matrix.py:81-101), in its order."""
+    from paper_1506_08938_b200 import SparseMatrix
+    from paper_1506_08938_b200.exceptions import DataDomainError, MatrixSizeError
+
+    def mk(indptr, rowidx, vals, rows=4, cols=3):
+        return SparseMatrix(rows, cols, indptr, rowidx, vals)
+
+    mk([0, 1, 2, 3], [0, 1, 3], [1.0, 2.0, 3.0])  # valid
+    mk([0, 0, 0, 0], [], [])  # empty is valid
+    cases = [
+        (MatrixSizeError, "column pointer array must have cols+1 entries",
+         ([0, 1, 3], [0, 1, 3], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "column pointers must span [0, nnz]",
+         ([1, 1, 2, 3], [0, 1, 3], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "column pointers must be non-decreasing",
+         ([0, 2, 1, 3], [0, 1, 3], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "row-index and value arrays must match",
+         ([0, 1, 2, 3], [0, 1], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "row index out of range", ([0, 1, 2, 3], [0, 4, 3], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "row index out of range", ([0, 1, 2, 3], [0, -1, 3], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "row indices not strictly increasing in column 1",
+         ([0, 1, 3, 3], [0, 2, 2], [1.0, 2.0, 3.0])),
+        (MatrixSizeError, "row indices not strictly increasing in column 2",
+         ([0, 1, 1, 3], [3, 3, 1], [1.0, 2.0, 3.0])),
+        (DataDomainError, "sparse values must be finite",
+         ([0, 1, 2, 3], [0, 1, 3], [1.0, float("nan"), 3.0])),
+        (DataDomainError, "stored sparse values must be > 0 (no explicit zeros)",
+         ([0, 1, 2, 3], [0, 1, 3], [1.0, 0.0, 3.0])),
+    ]
+    for typ, msg, args in cases:
+        with pytest.raises(typ) as ei:
+            mk(*args)
+        assert type(ei.value) is typ and str(ei.value) == msg, (msg, str(ei.value))
+    # a decreasing row across a column boundary is fine (column 0 ends at row 3)
+    mk([0, 2, 3, 3], [1, 3, 0], [1.0, 2.0, 3.0])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_host_containers_match_oracle_restatement(seed):
+    """Randomised triplets with duplicates, explicit zeros and cancelling
+    pairs: from_triplets / transpose / from_dense / to_dense agree bit for bit
+    with the oracle's restatement of matrix.py (pinned to the reference by
+    test_oracle_from_triplets_matches_reference)."""
+    from paper_1506_08938_b200 import DenseMatrix, SparseMatrix
+
+    rng = np.random.default_rng(seed)
+    rows, cols = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+    t = int(rng.integers(0, 300))
+    i = rng.integers(0, rows, t)
+    j = rng.integers(0, cols, t)
+    v = rng.choice([0.0, 1.0, 2.5, -2.5, 0.1, 0.2, 0.3], size=t) * rng.uniform(0.5, 2.0)
+    if seed % 2:
+        v = np.abs(v)  # nonnegative data: only cancellation-free sums
+    for sd in (True, False):
+        try:
+            want = orc.Csc.from_triplets(rows, cols, i, j, v, sum_duplicates=sd)
+            want_err = None
+        except ValueError as e:
+            want_err = (type(e).__name__, str(e))
+        try:
+            got = SparseMatrix.from_triplets(rows, cols, i, j, v, sum_duplicates=sd)
+            got_err = None
+        except ValueError as e:
+            got_err = (type(e).__name__, str(e))
+        if want_err is not None:
+            # argument errors: same message as the restatement
+            assert got_err is not None and got_err[1] == want_err[1]
+            continue
+        if got_err is not None:
+            # the restatement skips the constructor's validation; the product
+            # rejects exactly the outputs that break an invariant
+            dup = any((np.diff(want.indices[a:b]) <= 0).any()
+                      for a, b in zip(want.indptr[:-1], want.indptr[1:]))
+            if dup:
+                assert got_err[1].startswith("row indices not strictly increasing")
+            else:
+                assert (want.values <= 0).any()
+                assert got_err == ("DataDomainError",
+                                   "stored sparse values must be > 0 (no explicit zeros)")
+            continue
+        assert np.array_equal(got.indptr, want.indptr)
+        assert np.array_equal(got.indices, want.indices)
+        assert np.array_equal(got.values, want.values)
+        if not (got.values > 0).all():
+            continue
+        tw, tg = want.transpose(), got.transpose()
+        assert np.array_equal(tg.indptr, tw.indptr)
+        assert np.array_equal(tg.indices, tw.indices)
+        assert np.array_equal(tg.values, tw.values)
+        d = got.to_dense()
+        assert isinstance(d, DenseMatrix) and d.array.flags.f_contiguous
+        assert np.array_equal(d.array, want.to_dense())
+        back = SparseMatrix.from_dense(d)
+        assert np.array_equal(back.indptr, got.indptr)
+        assert np.array_equal(back.indices, got.indices)
+        assert np.array_equal(back.values, got.values)
+
+
+def test_dense_container_layout():
+    from paper_1506_08938_b200 import DenseMatrix
+    from paper_1506_08938_b200.exceptions import MatrixSizeError
+
+    a = np.arange(12.0).reshape(3, 4)
+    d = DenseMatrix(a)
+    assert d.array.flags.f_contiguous and (d.rows, d.cols) == (3, 4)
+    assert np.array_equal(d.data, a.reshape(-1, order="F"))
+    assert np.array_equal(d.column(2), a[:, 2])
+    f = np.asfortranarray(a)
+    assert DenseMatrix(f).array is f  # no copy for Fortran float64 input
+    c = d.copy()
+    c.array[0, 0] = -1.0
+    assert d.array[0, 0] == 0.0
+    z = DenseMatrix.zeros(2, 5)
+    assert z.array.shape == (2, 5) and z.array.flags.f_contiguous and not z.array.any()
+    with pytest.raises(MatrixSizeError, match="expected 2-D array, got ndim=1"):
+        DenseMatrix(np.ones(3))
+
+
 # ---------------------------------------------------------------------------
 # GPU
 # ---------------------------------------------------------------------------
