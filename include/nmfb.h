@@ -126,12 +126,26 @@ int nmfb_nnls_batch(int dtype, int mode, const void *Qa, const void *scale_a,
  * problems sharing one rescaled Hessian but each with its OWN stop state
  * (threshold max_stop, no fast-break sharing), fp64, reference order.
  * hist (nullable, count x hist_ld x 2 doubles): per-iteration squared
- * passive-gradient norm and rescaled objective, entry 0 = initial. */
+ * passive-gradient norm and rescaled objective, entry 0 = initial.
+ * check_gradients != 0: every iteration compares the incremental gradient
+ * with a fresh Q y + q (nqp.py:295-299); a drift beyond 1e-9 max(1, |fresh|)
+ * stops that problem with iters_out = -2. */
 int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_idx,
                    const uint8_t *active, int32_t r, const int32_t *ra_dev, const double *h,
                    double *x, int64_t count, double eps, int32_t max_inner, double max_stop,
                    int32_t *iters_out, double *final_out, double *hist, int32_t hist_ld,
-                   uint64_t *stats, void *stream);
+                   int32_t check_gradients, uint64_t *stats, void *stream);
+
+/* One step of the public NQP building blocks on `count` problems sharing a
+ * unit-diagonal Q (r x r fp64, row-major); x, grad (count x r) in, x_out,
+ * grad_out out (may alias x / grad).  fp64, one thread per problem.
+ *   NMFB_NQP_LINE_SEARCH: nqp.exact_line_search_step (nqp.py:151-183)
+ *   NMFB_NQP_GREEDY_CD:   nqp.greedy_cd_pass with `sweeps` updates
+ *                         (nqp.py:186-209; sweeps < 0 = r). */
+#define NMFB_NQP_LINE_SEARCH 0
+#define NMFB_NQP_GREEDY_CD 1
+int nmfb_nqp_step(int32_t op, const double *Q, int32_t r, const double *x, const double *grad,
+                  int64_t count, int32_t sweeps, double *x_out, double *grad_out, void *stream);
 
 /* Gram A^T A of A (rows, r) row-major (leading dim lda), accumulated in fp64
  * with a fixed (deterministic) summation order; out = full symmetric r x r
@@ -348,6 +362,11 @@ int nmfb_csc_to_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indp
 int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
                       const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
                       void *stream);
+
+/* Return the ingest kernels' cached scratch (a private stream-ordered pool on
+ * the current device, kept mapped between ingests) to the driver.  Waits for
+ * the device. */
+int nmfb_ingest_release_scratch(void);
 
 /* int64 -> int32 index narrowing (info[NMFB_INGEST_ROW_RANGE] = first
  * element that does not fit). */

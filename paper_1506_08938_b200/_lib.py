@@ -59,7 +59,8 @@ SIGNATURES = {
                                _i64, _i64, _f64, _vp, _i64, _i64, _f64, _i32, _f64, _vp, _vp, _vp,
                                _i32, _vp]),
     "nmfb_nqp_solve": (_int, [_vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i64, _f64, _i32, _f64,
-                              _vp, _vp, _vp, _i32, _vp, _vp]),
+                              _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
+    "nmfb_nqp_step": (_int, [_i32, _vp, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),
     "nmfb_gram_workspace_bytes": (_sz, [_i64, _i32]),
     "nmfb_gram": (_int, [_int, _vp, _i64, _i32, _i64, _vp, _vp, _vp]),
     "nmfb_gram_rescale": (_int, [_int, _vp, _i64, _i32, _i64, _vp, _vp, _f64, _vp, _vp, _vp, _vp,
@@ -102,6 +103,7 @@ SIGNATURES = {
                                       _vp, _vp, _vp]),
     "nmfb_csc_to_csr": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
     "nmfb_csc_validate": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp]),
+    "nmfb_ingest_release_scratch": (_int, []),
     "nmfb_narrow_indices": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "nmfb_sum_slots_rescale": (_int, [_int, _vp, _i32, _i64, _vp, _i32, _f64, _vp, _vp, _vp, _vp,
                                       _vp, _vp]),
@@ -166,7 +168,7 @@ def check(status, what):
 
 # kernels launched by one call of each entry point (gpu_launches accounting)
 KERNELS_PER_CALL = {
-    "nmfb_nnls_batch": 1, "nmfb_nqp_solve": 1, "nmfb_gram": 2, "nmfb_rescale": 1,
+    "nmfb_nnls_batch": 1, "nmfb_nqp_solve": 1, "nmfb_nqp_step": 1, "nmfb_gram": 2, "nmfb_rescale": 1,
     "nmfb_gemm_tall": 1, "nmfb_dense_linear_ref": 1, "nmfb_dense_yt_ref": 1, "nmfb_hp_ref": 1,
     "nmfb_csc_linear": 1, "nmfb_csr_yt": 1, "nmfb_dense_residual": 2, "nmfb_dot": 2,
     "nmfb_sum_parts": 1, "nmfb_dense_residual_kmajor": 2, "nmfb_csr_yt_chunked": 2, "nmfb_tc_gemm": 1, "nmfb_split_transpose": 1, "nmfb_transpose": 1,
@@ -174,6 +176,7 @@ KERNELS_PER_CALL = {
     "nmfb_tc_gemm_rows": 1, "nmfb_nnls_batch_peers": 1, "nmfb_peer_put": 1, "nmfb_peer_wait": 1,
     "nmfb_sum_slots_f64": 1, "nmfb_csc_from_triplets": 11, "nmfb_csc_to_csr": 8,
     "nmfb_csc_validate": 2, "nmfb_narrow_indices": 2, "nmfb_mur_update": 1,
+    "nmfb_ingest_release_scratch": 0,
     "nmfb_init_factors": 1, "nmfb_csc_segments": 1, "nmfb_chunk_segments": 1, "nmfb_sum_slots_rescale": 1,
     "nmfb_csc_linear_blocked": 1, "nmfb_csr_yt_chunked_blocked": 2,
 }

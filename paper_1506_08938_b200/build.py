@@ -19,12 +19,16 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libnmfb.so")
+# NMFB_BUILD_DIR / NMFB_EXTRA_FLAGS: an experiment variant of the library
+# built elsewhere (load it with NMFB_LIB_PATH); the default build is in-tree
+_VAR = os.environ.get("NMFB_BUILD_DIR")
+OBJ = os.path.join(_VAR, "obj") if _VAR else os.path.join(PKG, "_build")
+LIB = os.path.join(_VAR, "libnmfb.so") if _VAR else os.path.join(PKG, "libnmfb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "--expt-relaxed-constexpr", "-I", os.path.join(REPO, "include")]
+         "--expt-relaxed-constexpr", "-I", os.path.join(REPO, "include"),
+         *os.environ.get("NMFB_EXTRA_FLAGS", "").split()]
 
 
 def _headers():

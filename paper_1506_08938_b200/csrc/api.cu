@@ -38,6 +38,9 @@ int csc_to_csr_launch(int64_t rows, int64_t cols, int64_t nnz, const int64_t *in
 int csc_validate_launch(int64_t rows, int64_t cols, int64_t nnz, const int64_t *indptr,
                         const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
                         cudaStream_t st);
+int ingest_release_scratch();
+int nqp_step_launch(int op, const double *Q, int r, const double *x, const double *g,
+                    int64_t count, int sweeps, double *xo, double *go, cudaStream_t st);
 int narrow_indices_launch(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
                           cudaStream_t st);
 size_t gram_workspace_bytes(int64_t rows, int r);
@@ -216,7 +219,7 @@ int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_i
                    const uint8_t *active, int32_t r, const int32_t *ra_dev, const double *h,
                    double *x, int64_t count, double eps, int32_t max_inner, double max_stop,
                    int32_t *iters_out, double *final_out, double *hist, int32_t hist_ld,
-                   uint64_t *stats, void *stream) {
+                   int32_t check_gradients, uint64_t *stats, void *stream) {
     NnlsLaunch p;
     p.dtype = NMFB_F64;
     p.mode = NMFB_MODE_REFERENCE;
@@ -245,10 +248,17 @@ int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_i
     p.hist = hist;
     p.hist_ld = hist_ld;
     p.independent = true;
+    p.check_grad = check_gradients != 0;
     p.lanes = 0;
     p.stream = (cudaStream_t)stream;
     if (eps < 0.0 || eps > 1.0 || !stats || max_inner < 1) return NMFB_ERR_ARG;
     return check(nnls_launch(p));
+}
+
+int nmfb_nqp_step(int32_t op, const double *Q, int32_t r, const double *x, const double *grad,
+                  int64_t count, int32_t sweeps, double *x_out, double *grad_out, void *stream) {
+    return check(nqp_step_launch(op, Q, r, x, grad, count, sweeps, x_out, grad_out,
+                                 (cudaStream_t)stream));
 }
 
 size_t nmfb_gram_workspace_bytes(int64_t rows, int32_t r) { return gram_workspace_bytes(rows, r); }
@@ -477,6 +487,8 @@ int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *in
     return check(csc_validate_launch(rows, cols, nnz, indptr, rowidx, vals, vals_dtype, info,
                                      (cudaStream_t)stream));
 }
+
+int nmfb_ingest_release_scratch(void) { return check(ingest_release_scratch()); }
 
 int nmfb_narrow_indices(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
                         void *stream) {

@@ -189,30 +189,47 @@ __global__ void info_init_kernel(int64_t *info) {
     if (threadIdx.x < NMFB_INGEST_CODES) info[threadIdx.x] = INT64_MAX;
 }
 
+// Ingest scratch comes from a PRIVATE stream-ordered pool per device (the
+// process's default pool and PyTorch's allocator are left alone).  Its
+// release threshold keeps freed scratch mapped between ingests (threshold 0
+// would re-map GBs of scratch at every synchronisation: 10-400 ms host
+// stalls); nmfb_ingest_release_scratch() hands it back to the driver.
+constexpr int kMaxDevices = 64;
+static cudaMemPool_t g_pool[kMaxDevices];
+static bool g_pool_ok[kMaxDevices];
+
+static cudaMemPool_t ingest_pool(int dev) {
+    if (dev < 0 || dev >= kMaxDevices) return nullptr;
+    if (!g_pool_ok[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&g_pool[dev], &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        g_pool_ok[dev] = true;
+    }
+    return g_pool[dev];
+}
+
 struct Pool {
     cudaStream_t st;
+    cudaMemPool_t mp = nullptr;
     std::vector<void *> ptrs;
     explicit Pool(cudaStream_t s) : st(s) {
-        // keep freed scratch in the device's default pool instead of returning
-        // it to the driver at every synchronisation (the default threshold 0
-        // makes each ingest re-map its GBs of scratch: 10-400 ms host stalls)
-        static bool tuned = false;
-        if (!tuned) {
-            int dev = 0;
-            cudaMemPool_t pool;
-            if (cudaGetDevice(&dev) == cudaSuccess &&
-                cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t keep = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
-            cudaGetLastError();
-            tuned = true;
-        }
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) mp = ingest_pool(dev);
     }
     template <typename T>
     T *get(size_t n) {
         void *p = nullptr;
-        if (cudaMallocAsync(&p, n * sizeof(T) + 16, st) != cudaSuccess) return nullptr;
+        const size_t bytes = n * sizeof(T) + 16;
+        cudaError_t e = mp ? cudaMallocFromPoolAsync(&p, bytes, mp, st) : cudaMallocAsync(&p, bytes, st);
+        if (e != cudaSuccess) return nullptr;
         ptrs.push_back(p);
         return (T *)p;
     }
@@ -373,6 +390,16 @@ __global__ void narrow_kernel(const int64_t *__restrict__ in, int64_t n, int32_t
         if (x < INT32_MIN || x > INT32_MAX) flag(info, NMFB_INGEST_ROW_RANGE, t);
         out[t] = (int32_t)x;
     }
+}
+
+int ingest_release_scratch() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return NMFB_ERR_CUDA;
+    if (dev >= 0 && dev < kMaxDevices && g_pool_ok[dev]) {
+        if (cudaDeviceSynchronize() != cudaSuccess) return NMFB_ERR_CUDA;
+        if (cudaMemPoolTrimTo(g_pool[dev], 0) != cudaSuccess) return NMFB_ERR_CUDA;
+    }
+    return NMFB_OK;
 }
 
 int narrow_indices_launch(const int64_t *in, int64_t n, int32_t *out, int64_t *info,

@@ -32,6 +32,7 @@ struct NnlsLaunch {
     void *hist = nullptr;  // reference kernel: (count, hist_ld, 2) norm/objective history
     int hist_ld = 0;
     bool independent = false;
+    bool check_grad = false;  // reference kernel: fresh-gradient check every iteration
     int lanes;  // 0 = auto
     cudaStream_t stream;
     // fused all-gather (multi-GPU): every solution row is also stored at the

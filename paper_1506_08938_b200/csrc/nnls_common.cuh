@@ -29,6 +29,7 @@ struct NnlsArgs {
     T *hist;                 // nullable (count, hist_ld, 2): per-iteration (norm, objective)
     int hist_ld;             // reference kernel only (nqp.solve histories)
     bool independent;        // every problem its own fast-break scope (nqp.solve)
+    bool check_grad;         // reference kernel: nqp.solve(check_gradients=True), nqp.py:295-299
     unsigned long long *stats;  // [0] += inner iterations, [1] = min failing global index
     T *mirror[NMFB_MAX_PEERS];  // fast kernel: solution rows also stored here (peer GPUs)
     int nmirror;
@@ -70,6 +71,7 @@ static NnlsArgs<T, TH> make_args(const NnlsLaunch &p) {
     a.hist = (T *)p.hist;
     a.hist_ld = p.hist_ld;
     a.independent = p.independent;
+    a.check_grad = p.check_grad;
     a.stats = (unsigned long long *)p.stats;
     a.nmirror = p.nmirror;
     for (int q = 0; q < NMFB_MAX_PEERS; ++q) a.mirror[q] = q < p.nmirror ? (T *)p.mirror[q] : nullptr;

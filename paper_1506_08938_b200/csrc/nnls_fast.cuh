@@ -6,6 +6,15 @@
 
 // smallest E (coordinates per lane, L = 8) that uses the warp-shared Q
 // product q_times_w4
+// exact greedy-CD argmax (kernels.py:119); 0 = truncated-key experiment
+#ifndef NMFB_NNLS_EXACT_ARGMAX
+#define NMFB_NNLS_EXACT_ARGMAX 1
+#endif
+
+#ifndef NMFB_NNLS_YSMEM
+#define NMFB_NNLS_YSMEM 0
+#endif
+
 #ifndef NMFB_NNLS_W4_MIN_E
 #define NMFB_NNLS_W4_MIN_E 13
 #endif
@@ -100,35 +109,40 @@ __device__ __forceinline__ void q_times_f(float (&acc)[EE], F src, const float *
 
 // Q * src for the 4 problems of a warp (L = 8) with every Q element loaded
 // ONCE per warp and used for all 4 problems: lane l computes rows
-// k = e4 * 32 + l of all four problems (accumulators a[e4][p]); the four
-// source values of column j are four shuffles.  Each Q load is a 32-bit load
-// of the permuted layout (bank-conflict-free for LS/4 odd), so a column costs
-// 4 shuffles + ceil(R/32) loads instead of E 16-byte loads per group --
-// 2.6x fewer shared-memory wavefronts at r = 200.  The accumulators move
-// between the group layout (lane l of group g: rows e*8 + l of problem g) and
-// the warp layout through `scr` (the warp's four h staging rows, free after
-// the prologue).  Per row, the j order is the same as q_times_f's, so the
-// result is bit-identical to it with rot = 0.
+// k = e4 * 32 + l of all four problems (accumulators a[e4][p], packed in
+// pairs of problems for FFMA2); the four source values of column j are four
+// shuffles.  Each Q load is a 32-bit load of the permuted layout
+// (bank-conflict-free for LS/4 odd), so a column costs 4 shuffles +
+// ceil(R/32) loads instead of E 16-byte loads per group -- 2.6x fewer
+// shared-memory wavefronts at r = 200.  The accumulators move between the
+// group layout (lane l of group g: rows e*8 + l of problem g) and the warp
+// layout 32 rows at a time through `scr` (128 floats per warp): rows
+// e4*32 .. e4*32+31 are the elements e = 4 e4 .. 4 e4 + 3 of every group.
+// Per row, the j order is the same as q_times_f's, so the result is
+// bit-identical to it with rot = 0.
 template <int E, int EE, typename F>
 __device__ __forceinline__ void q_times_w4(float (&acc)[EE], F src, const float *Qs,
                                            float *scr, int r, int lane) {
     constexpr int L = 8, LS = nnls_ls(E), SP = L * LS;
     constexpr int E4 = (E * L + 31) / 32;
     const int l = lane & 7, g = lane >> 3;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int k = e * L + l;
-        if (k < r) scr[g * r + k] = acc[e];
-    }
-    __syncwarp();
-    float a[E4][4];
+    float2 a[E4][2];  // [e4][problem pair]: (p0, p1), (p2, p3)
 #pragma unroll
     for (int e4 = 0; e4 < E4; ++e4) {
-        const int k = e4 * 32 + lane;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) a[e4][p] = (k < r) ? scr[p * r + k] : 0.f;
+        for (int q = 0; q < 4; ++q) {
+            const int e = 4 * e4 + q;
+            if (e < E) scr[g * 32 + q * 8 + l] = acc[e];
+        }
+        __syncwarp();
+        const int k = e4 * 32 + lane;
+        float v[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) v[p] = (k < r) ? scr[p * 32 + lane] : 0.f;
+        a[e4][0] = make_float2(v[0], v[1]);
+        a[e4][1] = make_float2(v[2], v[3]);
+        __syncwarp();
     }
-    __syncwarp();
     const float *qcol = Qs + (lane & 7) * LS + (lane >> 3);  // + e4 * 4 + j * SP
 #pragma unroll 1
     for (int jl = 0; jl < L; ++jl) {
@@ -138,30 +152,32 @@ __device__ __forceinline__ void q_times_w4(float (&acc)[EE], F src, const float 
             float sp[4];
 #pragma unroll
             for (int p = 0; p < 4; ++p) sp[p] = __shfl_sync(NMFB_FULL_MASK, mine, 8 * p + jl);
+            const float2 s01 = make_float2(sp[0], sp[1]), s23 = make_float2(sp[2], sp[3]);
             const float *row = qcol + (je * L + jl) * SP;
 #pragma unroll
             for (int e4 = 0; e4 < E4; ++e4) {
                 const float q = row[e4 * 4];
-#pragma unroll
-                for (int p = 0; p < 4; ++p) a[e4][p] = fmaf(q, sp[p], a[e4][p]);
+                const float2 q2 = make_float2(q, q);
+                a[e4][0] = __ffma2_rn(q2, s01, a[e4][0]);
+                a[e4][1] = __ffma2_rn(q2, s23, a[e4][1]);
             }
         }
     }
 #pragma unroll
     for (int e4 = 0; e4 < E4; ++e4) {
-        const int k = e4 * 32 + lane;
-        if (k < r) {
+        scr[0 * 32 + lane] = a[e4][0].x;
+        scr[1 * 32 + lane] = a[e4][0].y;
+        scr[2 * 32 + lane] = a[e4][1].x;
+        scr[3 * 32 + lane] = a[e4][1].y;
+        __syncwarp();
 #pragma unroll
-            for (int p = 0; p < 4; ++p) scr[p * r + k] = a[e4][p];
+        for (int q = 0; q < 4; ++q) {
+            const int e = 4 * e4 + q;
+            // (rows k >= r read back exact zeros: zero sources, zero Q padding)
+            if (e < E) acc[e] = scr[g * 32 + q * 8 + l];
         }
+        __syncwarp();
     }
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int k = e * L + l;
-        if (k < r) acc[e] = scr[g * r + k];
-    }
-    __syncwarp();
 }
 
 // Q * src for the problems with `cond`: the warp-shared product for L = 8 at
@@ -214,6 +230,11 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     nnls_fast_kernel(NnlsArgs<float, TH> a) {
     constexpr int R = E * L;
     constexpr int EE = nnls_ee(E), EP = nnls_ep(E), LS = nnls_ls(E), SP = L * LS;
+    constexpr bool STAGE_H = E < NMFB_NNLS_W4_MIN_E;  // see the prologue
+    // y in shared memory during the greedy CD (experiment, default off:
+    // r = 200 1.84 -> 2.02 ms -- the per-selection y reload lengthens the
+    // dependency chain more than the removed owner select saves)
+    constexpr bool YSMEM = NMFB_NNLS_EXACT_ARGMAX && NMFB_NNLS_YSMEM;
     extern __shared__ __align__(16) float smem_f[];
     float *Qs = smem_f;                          // R x SP, permuted rows (see nnls_ep)
     __shared__ float blk_norm[B][32], blk_final[B][32];
@@ -273,8 +294,11 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         const bool valid = blk_live && (g >= a.index_base) && (j < a.count);
         const float m0 = (blk == blk0 && (a.index_base % 32) != 0) ? a.max_stop0 : 0.0f;
         const float *Qsl = Qs + l * LS;  // this lane's block of every row
-        // the warp's four h staging rows double as the q_times_w4 exchange buffer
-        float *wscr = smem_f + R * SP + (size_t)(warp * (32 / L)) * r;
+        // the warp's q_times_w4 exchange buffer (128 floats) and, in the CD
+        // phase, this problem's y row (lane l's coordinates at l*LS + e)
+        float *wscr = smem_f + R * SP + (size_t)warp * 128;
+        float *ys = smem_f + R * SP + (STAGE_H ? (size_t)32 * B * r : (size_t)128 * L * B) +
+                    (size_t)slot * SP + l * LS;
         // q_times source-lane rotation: one offset per quarter-warp (see q_times_f)
         // (measured: pays at E = 25, costs at E <= 13, where the per-lane source
         // lane and row offsets outweigh the saved shared-memory phases)
@@ -282,8 +306,10 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         // CD key mask (|dec| bits above the index code), kept in a register so the
         // per-coordinate key is a single LOP3 with the element code as immediate
         // (index_base < 2^62: the OR adds nothing, but ptxas cannot fold it)
+#if !NMFB_NNLS_EXACT_ARGMAX
         const unsigned kmask = (0x7FFFFFFFu & ~((1u << ((E * L <= 128) ? 7 : 8)) - 1u)) |
                                (unsigned)(a.index_base >> 62);
+#endif
 
         // register arrays padded to an even length (packed FP32x2 math); the
         // padding coordinates (k >= R) stay exactly zero
@@ -296,21 +322,42 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
 
         // ---- prologue: short-circuit, frozen check, compact load, gradient ----
         // The problem's full linear term h (sum of the split-K partials, loads
-        // issued 4 at a time) is staged once in shared memory: the short-circuit
-        // scan and the compact gather h[act_idx[k]] both read it from there.
+        // issued 4 at a time) is scanned for the short-circuit / frozen checks.
+        // Small E (STAGE_H): staged once in a shared-memory row that the
+        // compact gather h[act_idx[k]] reads back.  Large E: lane l holds
+        // h[e*L + l] in registers -- with every dimension active (ra == r,
+        // act_idx the identity) exactly the compact layout; otherwise
+        // h[act_idx[k]] is gathered again (an L1/L2 hit).
+        float hreg[STAGE_H ? 1 : EE];
         float *hrow = smem_f + R * SP + (size_t)slot * r;
         bool any_neg = false, frozen_neg = false;
-        if (valid) {
-            for (int i = l; i < r; i += L) {
-                const float hv = fast_h<TH>(a, j, i);
-                hrow[i] = hv;
-                if (hv < 0.f) {
-                    any_neg = true;
-                    if (!a.active[i]) frozen_neg = true;
+        if constexpr (STAGE_H) {
+            if (valid) {
+                for (int i = l; i < r; i += L) {
+                    const float hv = fast_h<TH>(a, j, i);
+                    hrow[i] = hv;
+                    if (hv < 0.f) {
+                        any_neg = true;
+                        if (!a.active[i]) frozen_neg = true;
+                    }
+                }
+            }
+            __syncwarp(gmask);
+        } else {
+#pragma unroll
+            for (int e = 0; e < EE; ++e) {
+                const int i = e * L + l;
+                hreg[e] = 0.f;
+                if (valid && i < r) {
+                    const float hv = fast_h<TH>(a, j, i);
+                    hreg[e] = hv;
+                    if (hv < 0.f) {
+                        any_neg = true;
+                        if (!a.active[i]) frozen_neg = true;
+                    }
                 }
             }
         }
-        __syncwarp(gmask);
         any_neg = gany<L>(any_neg, gmask, gbase);
         frozen_neg = gany<L>(frozen_neg, gmask, gbase);
         if (valid) {
@@ -321,14 +368,20 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
             }
         }
         const bool solve = valid && any_neg && !frozen_neg;
+        const bool ident = (ra == r);
 #pragma unroll
         for (int e = 0; e < EE; ++e) {
             const int k = e * L + l;
             float qv = 0.f, yv = 0.f;
             if (solve && k < ra) {
-                const int ik = act_s[k];
+                const int ik = ident ? k : act_s[k];
                 const float sv = scl_s[k];
-                qv = __fdiv_rn(hrow[ik], sv);
+                float hv;
+                if constexpr (STAGE_H)
+                    hv = hrow[ik];
+                else
+                    hv = ident ? hreg[e] : fast_h<TH>(a, j, ik);
+                qv = __fdiv_rn(hv, sv);
                 yv = a.x[j * r + ik] * sv;
             }
             y[e] = yv;
@@ -514,25 +567,98 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
             }
             }
             if (running) {
-                // Greedy CD (kernels.py:106-132).  The argmax is an integer max
-                // over packed keys: |dec| with its low IB bits replaced by an
-                // index code, (EMAX - e) << LB | (L - 1 - l), so equal truncated
-                // decreases resolve to the lowest coordinate k = e*L + l (strict >,
-                // kernels.py:119).  The lane part is OR-ed in after the in-lane
-                // 3-way tree, so the per-coordinate key is one LOP3 (mask in a
-                // register, element code an immediate).
-                constexpr int IB = (R <= 128) ? 7 : 8;
-                constexpr unsigned IMASK = (1u << IB) - 1u;
                 constexpr int LB = (L == 1) ? 0 : (L == 2) ? 1 : (L == 4) ? 2 : (L == 8) ? 3
                                  : (L == 16) ? 4 : 5;
-                constexpr int EB = IB - LB;
-                constexpr unsigned EMAXC = (1u << EB) - 1u;
-                static_assert(EE <= (1 << EB), "index code does not fit the key");
                 const unsigned lcode = (unsigned)(L - 1 - l);
                 int pp = -1;
                 float pdx = 0.f;
+                if constexpr (YSMEM) {
+                    // y lives in this problem's shared-memory row for the CD
+                    // phase: the winner's owner lane updates its coordinate with
+                    // one indexed store instead of a select over its E registers
+#pragma unroll
+                    for (int q = 0; q < EP / 4; ++q)
+                        reinterpret_cast<float4 *>(ys)[q] =
+                            make_float4(4 * q < EE ? y[4 * q] : 0.f, 4 * q + 1 < EE ? y[4 * q + 1] : 0.f,
+                                        4 * q + 2 < EE ? y[4 * q + 2] : 0.f,
+                                        4 * q + 3 < EE ? y[4 * q + 3] : 0.f);
+                }
                 for (int s = 0; s < ra; ++s) {
                     if (s > 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
+                    int ep, lp;
+                    float dwin = 0.f;
+#if NMFB_NNLS_EXACT_ARGMAX
+                    // Greedy CD (kernels.py:106-132) with the reference's exact
+                    // argmax: the largest |dec| wins and equal values go to the
+                    // lowest coordinate k = e*L + l (strict >, kernels.py:119).
+                    // dec = d (g + d/2) with d = -min(g, y) is <= 0 for every
+                    // coordinate, so its raw bit pattern orders by |dec| as an
+                    // unsigned integer (+-0 lowest).  In-lane: a pair tree over
+                    // (bits, e[, d]) keeping the lower e on equality; across the
+                    // group: a max over bits << 32 | code(e, l), lower (e, l) =
+                    // higher code.
+                    float yv[YSMEM ? EP : 1];
+                    if constexpr (YSMEM) {
+#pragma unroll
+                        for (int q = 0; q < EP / 4; ++q) {
+                            const float4 v = reinterpret_cast<const float4 *>(ys)[q];
+                            yv[4 * q] = v.x;
+                            yv[4 * q + 1] = v.y;
+                            yv[4 * q + 2] = v.z;
+                            yv[4 * q + 3] = v.w;
+                        }
+                    }
+                    auto ycur = [&](int e) { if constexpr (YSMEM) return yv[e]; else return y[e]; };
+                    unsigned key[EE];
+                    int ix[EE];
+                    float dv[YSMEM ? EE : 1];
+#pragma unroll
+                    for (int e = 0; e < EE; e += 2) {
+                        const float d0 = -fminf(gr[e], ycur(e)), d1 = -fminf(gr[e + 1], ycur(e + 1));
+                        const float2 t = __ffma2_rn(make_float2(0.5f, 0.5f), make_float2(d0, d1),
+                                                    make_float2(gr[e], gr[e + 1]));
+                        const float2 dc = __fmul2_rn(make_float2(d0, d1), t);
+                        key[e] = __float_as_uint(dc.x);
+                        key[e + 1] = __float_as_uint(dc.y);
+                        ix[e] = e;
+                        ix[e + 1] = e + 1;
+                        if constexpr (YSMEM) {
+                            dv[e] = d0;
+                            dv[e + 1] = d1;
+                        }
+                    }
+#pragma unroll
+                    for (int w = 1; w < EE; w *= 2)
+#pragma unroll
+                        for (int e = 0; e + w < EE; e += 2 * w) {
+                            const bool keep = key[e] >= key[e + w];
+                            key[e] = keep ? key[e] : key[e + w];
+                            ix[e] = keep ? ix[e] : ix[e + w];
+                            if constexpr (YSMEM) dv[e] = keep ? dv[e] : dv[e + w];
+                        }
+                    if constexpr (YSMEM) dwin = dv[0];
+                    unsigned long long kb = ((unsigned long long)key[0] << 32) |
+                                            ((unsigned)(EE - 1 - ix[0]) << LB) | lcode;
+#pragma unroll
+                    for (int o = L / 2; o > 0; o >>= 1) {
+                        const unsigned long long other = __shfl_xor_sync(gmask, kb, o, L);
+                        kb = other > kb ? other : kb;
+                    }
+                    if (((unsigned)(kb >> 32) & 0x7FFFFFFFu) == 0u) {
+                        pp = -1;
+                        break;
+                    }
+                    ep = (EE - 1) - (int)((unsigned)kb >> LB);
+                    lp = (L - 1) - (int)((unsigned)kb & (unsigned)(L - 1));
+#else
+                    // truncated-key argmax (experiment): |dec| with its low IB bits
+                    // replaced by an index code -- decreases within ~2^-15 of each
+                    // other resolve to the lower index
+                    constexpr int IB = (R <= 128) ? 7 : 8;
+                    constexpr unsigned IMASK = (1u << IB) - 1u;
+                    constexpr int EB = IB - LB;
+                    constexpr unsigned EMAXC = (1u << EB) - 1u;
+                    static_assert(EE <= (1 << EB), "index code does not fit the key");
                     unsigned key[EE];
 #pragma unroll
                     for (int e = 0; e < EE; e += 2) {
@@ -560,48 +686,39 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                         pp = -1;
                         break;
                     }
-                    const int ep = (int)(EMAXC - ((kb & IMASK) >> LB));
-                    const int lp = (int)((unsigned)(L - 1) - (kb & (unsigned)(L - 1)));
-                    float dxo = 0.f;
-#ifndef NMFB_NNLS_OWNER_SWITCH
-#define NMFB_NNLS_OWNER_SWITCH 0
+                    ep = (int)(EMAXC - ((kb & IMASK) >> LB));
+                    lp = (int)((unsigned)(L - 1) - (kb & (unsigned)(L - 1)));
 #endif
-#if NMFB_NNLS_OWNER_SWITCH
-                    if (l == lp) {
-                        // the owner lane updates its coordinate ep (a jump table
-                        // instead of a compare/select over all E registers)
-                        switch (ep) {
-#define NMFB_OWN(N)                                                      \
-        case N:                                                              \
-            if (N < E) {                                                     \
-                dxo = -fminf(gr[N < EE ? N : 0], y[N < EE ? N : 0]);         \
-                y[N < EE ? N : 0] += dxo;                                    \
-            }                                                                \
-            break;
-                            NMFB_OWN(0) NMFB_OWN(1) NMFB_OWN(2) NMFB_OWN(3) NMFB_OWN(4) NMFB_OWN(5)
-                            NMFB_OWN(6) NMFB_OWN(7) NMFB_OWN(8) NMFB_OWN(9) NMFB_OWN(10) NMFB_OWN(11)
-                            NMFB_OWN(12) NMFB_OWN(13) NMFB_OWN(14) NMFB_OWN(15) NMFB_OWN(16)
-                            NMFB_OWN(17) NMFB_OWN(18) NMFB_OWN(19) NMFB_OWN(20) NMFB_OWN(21)
-                            NMFB_OWN(22) NMFB_OWN(23) NMFB_OWN(24) NMFB_OWN(25) NMFB_OWN(26)
-                            NMFB_OWN(27) NMFB_OWN(28) NMFB_OWN(29) NMFB_OWN(30) NMFB_OWN(31)
-#undef NMFB_OWN
-                            default: break;
-                        }
-                    }
-#else
+                    if constexpr (YSMEM) {
+                        // the winner's step, carried through the argmax tree:
+                        // d = -min(g, y) of the winning coordinate
+                        pdx = (L == 1) ? dwin : __shfl_sync(gmask, dwin, lp, L);
+                        if (l == lp) ys[ep] += pdx;
+                    } else {
+                        float dxo = 0.f;
 #pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        if (e == ep && l == lp) {
-                            dxo = -fminf(gr[e], y[e]);
-                            y[e] += dxo;
+                        for (int e = 0; e < E; ++e) {
+                            if (e == ep && l == lp) {
+                                dxo = -fminf(gr[e], y[e]);
+                                y[e] += dxo;
+                            }
                         }
+                        pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, lp, L);
                     }
-#endif
                     moved = true;
-                    pdx = (L == 1) ? dxo : __shfl_sync(gmask, dxo, lp, L);
                     pp = ep * L + lp;
                 }
                 if (pp >= 0) axpy_row<EE, EP>(gr, Qsl + pp * SP, pdx);
+                if constexpr (YSMEM) {
+#pragma unroll
+                    for (int q = 0; q < EP / 4; ++q) {
+                        const float4 v = reinterpret_cast<const float4 *>(ys)[q];
+                        if (4 * q < EE) y[4 * q] = v.x;
+                        if (4 * q + 1 < EE) y[4 * q + 1] = v.y;
+                        if (4 * q + 2 < EE) y[4 * q + 2] = v.z;
+                        if (4 * q + 3 < EE) y[4 * q + 3] = v.w;
+                    }
+                }
                 iters += 1;
                 bool finite = true;
                 float nk = 0.f;
@@ -696,8 +813,14 @@ template <typename TH, int E, int L, int B>
 static int launch_fast_variant(const NnlsLaunch &p) {
     auto a = make_args<float, TH>(p);
     constexpr int R = E * L, SP = L * nnls_ls(E);
-    // Q (R x SP, permuted rows) + one staged h row (r floats) per problem slot
-    size_t smem = sizeof(float) * ((size_t)R * SP + (size_t)32 * B * p.r);
+    // Q (R x SP, permuted rows) + small E: one staged h row (r floats) per
+    // problem slot; large E: a 128-float q_times_w4 exchange buffer per warp;
+    // + one y row (SP floats) per problem slot for the greedy CD
+    constexpr bool STAGE_H = E < NMFB_NNLS_W4_MIN_E;
+    constexpr bool YSMEM = NMFB_NNLS_EXACT_ARGMAX && NMFB_NNLS_YSMEM;
+    size_t smem = sizeof(float) * ((size_t)R * SP + (STAGE_H ? (size_t)32 * B * p.r
+                                                              : (size_t)128 * L * B) +
+                                   (YSMEM ? (size_t)32 * B * SP : 0));
 
     auto kern = nnls_fast_kernel<TH, E, L, B, false>;
     if (p.nmirror > 0) {

@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(64) nnls_ref_kernel(NnlsArgs<T, TH> a) {
 
     T hbuf[MAXR], y[MAXR], grad[MAXR], d[MAXR], ynew[MAXR], delta[MAXR], qd[MAXR];
     int status = ST_DONE;
-    bool fail = false, write_x = false;
+    bool fail = false, write_x = false, gdrift = false;
     int iters = 0;
     T final_norm = T(0), norm_k = T(0), threshold = T(0);
     const T *Q = a.Qa;
@@ -186,8 +186,23 @@ __global__ void __launch_bounds__(64) nnls_ref_kernel(NnlsArgs<T, TH> a) {
             bool finite = true;
             for (int i = 0; i < ra; ++i)
                 if (!(is_finite(y[i]) && is_finite(grad[i]))) finite = false;
-            if (!finite) {
+            bool drift = false;
+            if (finite && a.check_grad) {
+                // nqp.py:295-299: the incremental gradient against a fresh
+                // Q y + q, every iteration
+                T ref = T(1), worst = T(0);
+                for (int k = 0; k < ra; ++k) {
+                    T acc = O::div(hbuf[a.act_idx[k]], a.scale_a[k]);
+                    for (int jj = 0; jj < ra; ++jj) acc = O::madd(acc, Q[k * ra + jj], y[jj]);
+                    if (fabs(acc) > ref) ref = fabs(acc);
+                    const T e = fabs(O::sub(grad[k], acc));
+                    if (e > worst) worst = e;
+                }
+                drift = worst > O::mul(T(1e-9), ref);
+            }
+            if (!finite || drift) {
                 fail = true;
+                gdrift = drift;
                 write_x = false;
                 status = ST_DONE;
                 final_norm = T(0);
@@ -212,7 +227,9 @@ __global__ void __launch_bounds__(64) nnls_ref_kernel(NnlsArgs<T, TH> a) {
             for (int i = 0; i < r; ++i) a.x[j * r + i] = T(0);
             for (int k = 0; k < ra; ++k) a.x[j * r + a.act_idx[k]] = O::div(y[k], a.scale_a[k]);
         }
-        if (a.iters_out) a.iters_out[j] = fail ? -1 : iters;
+        // -1: non-finite iterate / frozen-dimension failure; -2: the
+        // check_gradients drift test failed (the caller raises AssertionError)
+        if (a.iters_out) a.iters_out[j] = fail ? (gdrift ? -2 : -1) : iters;
         if (a.final_out) a.final_out[j] = fail ? T(0) : final_norm;
         if (fail) atomicMin((unsigned long long *)&a.stats[1], (unsigned long long)g);
     }

@@ -385,6 +385,8 @@ class CudaEngine:
         K = self.iters_done
         L.call("nmfb_sum_slots_f64", D.vp(self.piece_slots), px.world, K * 12,
                self.st.max_iters * 12, D.vp(self.st.pieces), D.stream_handle())
+        # a timed-out epoch wait left stale slots behind: fail the fit loudly
+        px.check()
 
     def objective_pieces(self, k, yt_rows, lo, hi):
         """Additive per-rank pieces (slot layout of device.Alternation):
@@ -460,16 +462,39 @@ class DistFit:
         G0, FT0 = init
         self.engine = CudaEngine(X_block, cfg, G0, FT0, cfg.max_outer, m)
         self.peer = False
-        if peer_wanted(self.engine):
-            try:
-                self.engine.enable_peer(self.plan, group)
-                self.peer = True
-            except Exception as exc:  # no peer access / symmetric memory: NCCL
-                self.peer_error = f"{type(exc).__name__}: {exc}"
+        if peer_agreed(self.engine, group):
+            # every rank is eligible with the same slot layout: the rendezvous
+            # below is entered by all ranks or by none; a failure past this
+            # point is an error on that rank (no silent per-rank fallback)
+            self.engine.enable_peer(self.plan, group)
+            self.peer = True
         if not self.peer:
             self.engine.bind_plan(self.plan)
         self.state = _StateView(DistAlternation(self.engine, self.plan, rank, group),
                                 self.engine.st)
+
+
+def peer_agreed(engine, group=None):
+    """The peer path is taken only when EVERY rank is eligible and every
+    rank derived the same partial-slot count P (the symmetric regions'
+    offsets depend on it): an all-gather of (eligible, P) decides it
+    collectively, so no rank waits in the symmetric-memory rendezvous while
+    another falls back to NCCL."""
+    ok = peer_wanted(engine)
+    if ok:
+        try:  # local prerequisites, checked before the collective decision
+            import torch.distributed._symmetric_memory  # noqa: F401
+        except Exception:
+            ok = False
+    P = int(getattr(engine.st, "splits_m", 0)) if ok else 0
+    if not (dist.is_initialized() and dist.get_backend(group) == "nccl"):
+        return False
+    dev = engine.data.device
+    mine = torch.tensor([1 if ok else 0, P], dtype=torch.int64, device=dev)
+    alls = [torch.empty_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(alls, mine, group=group)
+    got = torch.stack(alls).cpu()
+    return bool(got[:, 0].min().item() == 1 and (got[:, 1] == got[0, 1]).all().item())
 
 
 def peer_wanted(engine):

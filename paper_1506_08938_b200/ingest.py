@@ -56,6 +56,13 @@ def _device():
     return require_cuda()
 
 
+def release_scratch():
+    """Hand the ingest kernels' cached scratch (kept mapped between ingests to
+    avoid re-mapping GBs per call) back to the driver (nmfb_ingest_release_scratch)."""
+    _device()
+    L.call("nmfb_ingest_release_scratch")
+
+
 def raise_for(info, codes=_ORDER):
     """Raise the reference's exception for the first failing check in `info`
     (host int64 array of NMFB_INGEST_CODES entries)."""

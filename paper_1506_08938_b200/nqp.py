@@ -154,13 +154,62 @@ def _passive_norm_sq(x, grad):
     return float(d @ d)
 
 
+def _device_step(op, Q, x, grad, sweeps=-1):
+    """nmfb_nqp_step on the GPU for one problem (1-D x, grad) or a batch of
+    problems sharing Q (rows of 2-D x, grad)."""
+    import torch
+
+    from . import _lib as L
+    from . import device as D
+
+    dev = D.require_cuda()
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    x = np.asarray(x, dtype=np.float64)
+    grad = np.asarray(grad, dtype=np.float64)
+    r = Q.shape[0]
+    if Q.shape != (r, r) or x.shape[-1] != r or grad.shape != x.shape or x.ndim > 2:
+        raise ValueError("Q must be r x r and x, grad (r,) or (count, r) alike")
+    if r == 0:
+        return x.copy(), grad.copy()
+    xs, gs = np.atleast_2d(x), np.atleast_2d(grad)
+    Qd = torch.from_numpy(Q).to(dev)
+    xd = torch.from_numpy(np.ascontiguousarray(xs)).to(dev)
+    gd = torch.from_numpy(np.ascontiguousarray(gs)).to(dev)
+    L.call("nmfb_nqp_step", op, D.vp(Qd), r, D.vp(xd), D.vp(gd), xs.shape[0], int(sweeps),
+           D.vp(xd), D.vp(gd), D.stream_handle())
+    xo, go = xd.cpu().numpy(), gd.cpu().numpy()
+    return (xo[0], go[0]) if x.ndim == 1 else (xo, go)
+
+
+def exact_line_search_step(Q, q, x, grad):
+    """One projected exact-line-search step along the passive-set gradient
+    (nqp.py:151-183), on the GPU: alpha = |d|^2 / d'Qd (1 if the curvature is
+    not positive), the projected point, the gradient updated over the changed
+    coordinates, and the shortened step at the first breakpoint when the
+    projection would increase the objective.  ``q`` is implicit in ``grad``
+    (kept for the reference's signature).  x, grad may also be (count, r)
+    batches sharing Q."""
+    return _device_step(0, Q, x, grad)
+
+
+def greedy_cd_pass(Q, q, x, grad, sweeps=None):
+    """``sweeps`` (default r) greedy coordinate-descent updates (nqp.py:186-209)
+    on the GPU: the clamped minimiser of the coordinate with the largest
+    decrease (ties to the lowest index), unit-diagonal Q.  Batched like
+    ``exact_line_search_step``."""
+    if sweeps is not None and sweeps < 0:
+        raise ValueError("sweeps must be >= 0")
+    return _device_step(1, Q, x, grad, -1 if sweeps is None else int(sweeps))
+
+
 def solve(p: NqpProblem, stop: StopState | None = None, max_inner: int = DEFAULT_MAX_INNER,
           check_gradients: bool = False) -> NqpSolution:
     """Solve an NQP problem to the accuracy governed by ``stop`` (nqp.py:217-320).
 
     The iterative solve runs on the GPU (reference-order fp64 kernel).
-    ``check_gradients`` verifies the final incremental gradient against a
-    fresh Q y + q (the reference checks every iteration).
+    ``check_gradients`` compares the incremental gradient with a fresh
+    Q y + q after every inner iteration inside the kernel (nqp.py:295-299)
+    and raises AssertionError at the first drift beyond 1e-9.
     """
     import torch
 
@@ -204,8 +253,11 @@ def solve(p: NqpProblem, stop: StopState | None = None, max_inner: int = DEFAULT
     L.call("nmfb_nqp_solve", D.vp(bufs["Qa"]), D.vp(bufs["sa"]), D.vp(bufs["act"]),
            D.vp(bufs["active"]), r, D.vp(bufs["ra"]), D.vp(h), D.vp(x), 1,
            float(stop.epsilon), int(max_inner), float(stop.max_stop), D.vp(iters), D.vp(final),
-           D.vp(hist), max_inner + 1, D.vp(stats), D.stream_handle())
+           D.vp(hist), max_inner + 1, 1 if check_gradients else 0, D.vp(stats),
+           D.stream_handle())
     it = int(iters.item())
+    if it == -2:
+        raise AssertionError("incremental gradient drifted from Qx + q")
     if it < 0:
         raise NumericalFailureError(f"NaN/Inf after inner iterations (max {max_inner})",
                                     last_x=p.x0.copy())
@@ -213,15 +265,6 @@ def solve(p: NqpProblem, stop: StopState | None = None, max_inner: int = DEFAULT
     hh = hist.cpu().numpy()[: it + 1]
     norm0 = float(hh[0, 0])
     norm_k = float(final.item())
-    if check_gradients:
-        idx = np.flatnonzero(active)
-        y = xs[idx] * scale[idx]
-        qa = p.h[idx] / scale[idx]
-        fresh = Qa @ y + qa
-        gy = (p.H @ xs + p.h)[idx] / scale[idx]
-        ref = max(1.0, float(np.max(np.abs(fresh))))
-        if np.max(np.abs(gy - fresh)) > 1e-9 * ref:
-            raise AssertionError("incremental gradient drifted from Qx + q")
     stop.update(norm_k)
     return NqpSolution(x=xs, grad=p.H @ xs + p.h, inner_iterations=it,
                        initial_passive_grad_norm_sq=norm0, final_passive_grad_norm_sq=norm_k,
@@ -288,15 +331,15 @@ def solve_batch(H, h, x0=None, epsilon=DEFAULT_EPSILON, max_inner=DEFAULT_MAX_IN
     StopState(epsilon, max_stop)  # argument validation
     if max_inner < 1:
         raise ValueError("max_inner must be >= 1")
-    grad0 = x0 @ H.T + h
+    # the KKT short-circuit (nqp.py:241-253) is an exact-zero test: every row
+    # with a nonzero warm start gets the same matrix-vector product ``solve``
+    # computes (H @ x0 + h), so its decision is bit-identical; a zero warm
+    # start has grad0 = h exactly
+    grad0 = h.copy()
+    for k in np.flatnonzero(np.any(x0 != 0.0, axis=1)):
+        grad0[k] = H @ x0[k] + h[k]
     pas = (x0 > 0) | (grad0 < 0)
     norm0 = np.einsum("ij,ij->i", np.where(pas, grad0, 0.0), np.where(pas, grad0, 0.0))
-    # the KKT short-circuit is an exact-zero test: decide near-zero rows with
-    # the same matrix-vector product ``solve`` uses (nqp.py:241-253)
-    tiny = np.flatnonzero(norm0 <= 1e-20 * (1.0 + np.max(np.abs(grad0), axis=1)) ** 2)
-    for k in tiny:
-        grad0[k] = H @ x0[k] + h[k]
-        norm0[k] = _passive_norm_sq(x0[k], grad0[k])
     zero_h = np.all(h >= 0.0, axis=1)
     kkt = ~zero_h & (norm0 == 0.0)
     run = np.flatnonzero(~zero_h & ~kkt)
@@ -336,7 +379,7 @@ def solve_batch(H, h, x0=None, epsilon=DEFAULT_EPSILON, max_inner=DEFAULT_MAX_IN
         L.call("nmfb_nqp_solve", D.vp(bufs["Qa"]), D.vp(bufs["sa"]), D.vp(bufs["act"]),
                D.vp(bufs["active"]), r, D.vp(bufs["ra"]), D.vp(hd), D.vp(xd), int(run.size),
                float(epsilon), int(max_inner), float(max_stop), D.vp(it_d), D.vp(fin_d),
-               D.vp(hist), hl, D.vp(stats), D.stream_handle())
+               D.vp(hist), hl, 0, D.vp(stats), D.stream_handle())
         it = it_d.cpu().numpy().astype(np.int64)
         if np.any(it < 0):
             k = int(run[np.flatnonzero(it < 0)[0]])
@@ -352,7 +395,11 @@ def solve_batch(H, h, x0=None, epsilon=DEFAULT_EPSILON, max_inner=DEFAULT_MAX_IN
             for t, k in enumerate(run):
                 nh[k, : it[t] + 1] = hh[t, : it[t] + 1, 0]
                 oh[k, : it[t] + 1] = hh[t, : it[t] + 1, 1]
-    return NqpBatchSolution(x=x, grad=x @ H.T + h, inner_iterations=iters,
+    # final gradient per problem as ``solve`` forms it (H @ x + h)
+    grad = h.copy()
+    for k in np.flatnonzero(np.any(x != 0.0, axis=1)):
+        grad[k] = H @ x[k] + h[k]
+    return NqpBatchSolution(x=x, grad=grad, inner_iterations=iters,
                             initial_passive_grad_norm_sq=init,
                             final_passive_grad_norm_sq=final,
                             passive_grad_norm_history=nh, objective_history=oh)
