@@ -1,24 +1,26 @@
 """Benchmark of the alternating-NNLS hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2|3|4|5]
 
-Workload (BASELINE.json configs[1], "C2"): dense NMF of X = W0 H0 + |N(0,0.05)|,
-X 10000 x 20000, W0/H0 ~ Exp(1) (seed 1), rank 50, fp32 on the GPU.  One step
-= one outer iteration of nmf.fit (Gram + rescale, G^T X, NNLS over the
-20000 columns, F F^T, X F^T, NNLS over the 10000 rows, objective), i.e.
-30000 column/row NNLS solves.  ``value`` = solves/s over the timed steps with
-X and the factors resident in HBM; ``e2e`` = the same metric through the
-public ``fit()`` call from a pinned host buffer (upload of X, seeded init,
-the iterations, download of G, F and the log all inside the timed region).
+Default workload (BASELINE.json configs[4], "C5", the config its metric is
+quoted on "at 1/2/4/8 B200"): sparse text-like NMF, X 1000000 x 200000 CSC at
+0.05% density (Zipf rows/columns, tf-idf-scaled Poisson counts, seed 4),
+rank 200, fp32 on the GPU.  One step = one outer iteration of nmf.fit (Gram +
+rescale, G^T X, NNLS over the 200000 columns, F F^T, X F^T, NNLS over the
+1000000 rows, objective by the trace identity), i.e. 1.2 M column/row NNLS
+solves.  ``value`` = solves/s over the timed steps with X and the factors
+resident in HBM; ``e2e`` = the same metric through the public ``fit()`` call
+from the reference's own host input (a float64 SparseMatrix / ndarray):
+upload, device CSR build, seeded init, the config's iterations, download of
+G, F and the log, all inside the timed region.
 
 --config 3|5 (sparse) at N > 1: strong scaling -- the config's matrix is
 split into the shard plan's 32-aligned column blocks (BASELINE: "columns
-sharded across 1/2/4/8 GPUs").
-
-N > 1 (torchrun, one rank per GPU, dense): weak scaling -- every rank owns a
-C2-shaped column block of a 10000 x (20000 N) matrix (columns sharded, G
-replicated, NCCL for the r x r Gram allreduce, the Y^T reduce-scatter and the
-G allgather; paper_1506_08938_b200/dist.py).
+sharded across 1/2/4/8 GPUs").  --config 2|4 (dense) at N > 1: weak scaling
+-- every rank owns a config-shaped column block (G replicated; the r x r Gram
+allreduce, the Y^T reduce-scatter and the G allgather as NVLink peer stores
+or NCCL; paper_1506_08938_b200/dist.py).
 
 ``--impl reference``: the reference's CPU path on this host's cores -- the
 oracle port (oracle/, a C + numpy restatement bit-exact to the reference),
@@ -49,9 +51,11 @@ WORKLOADS = {
     4: "C4: dense L1/L2-regularised NMF 20000x20000, rank 64, mu1=0.1, beta2=0.01, fp32 "
        "(BASELINE.json configs[3])",
     5: "C5: sparse text-like NMF 1000000x200000 CSC 0.05%, rank 200, fp32 (BASELINE.json "
-       "configs[4]), single-GPU leg",
+       "configs[4])",
 }
-FP32_TFLOPS = 148 * 128 * 2 * 1965e6 / 1e12  # FFMA peak from the measured max SM clock
+# bounded CPU-baseline samples: outer iterations of the oracle port per config
+# (~10-25 s of host work on a 16-core box)
+CPU_SAMPLE_ITERS = {2: 4, 3: 12, 4: 2, 5: 1}
 
 
 def parse():
@@ -62,9 +66,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
-                   help="BASELINE.json config (default 2 = configs[1], the headline workload); "
-                        "3-5 are measured here too (sparse 3/5 at N = 1)")
+    p.add_argument("--config", type=int, default=5, choices=[2, 3, 4, 5],
+                   help="BASELINE.json config (default 5 = configs[4], the largest config, "
+                        "on which the metric is quoted at 1/2/4/8 GPUs)")
     return p.parse_args()
 
 
@@ -194,21 +198,36 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic(kernel="nmfb_tc_gemm"):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed ncu --set full capture (profiles/traffic_r*.json, newest
-    round), or None."""
+def micro_peaks():
+    """CUDA-core FMA and L2 read peaks measured on a B200 by tests/micro
+    (profiles/r02_micro_peaks.json); spec-derived fallbacks otherwise."""
+    path = os.path.join(REPO, "profiles", "r02_micro_peaks.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return (float(d["ffma_tflops"]), float(d["l2_stream_read_gbs"]),
+                "measured (tests/micro/fma_peak.cu, l2_bw.cu; profiles/r02_micro_peaks.json)")
+    except (OSError, ValueError, KeyError):
+        return 148 * 128 * 2 * 1965e6 / 1e12, None, "spec-derived (148 SM x 128 FMA x 2 x 1965 MHz)"
+
+
+def profile_traffic(cid, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at
+    config `cid` from the committed ncu --set full captures
+    (profiles/traffic_r*.json, newest round first: {"C5": {kernel: {...}}}),
+    or None."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(REPO, "profiles", "traffic_r*.json")))
-    if not files:
-        return None
-    try:
-        with open(files[-1]) as f:
-            k = json.load(f).get(kernel)
-        return None if k is None else int(k["dram_bytes_read"]) + int(k["dram_bytes_write"])
-    except (OSError, ValueError, KeyError, TypeError):
-        return None
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "traffic_r*.json")),
+                       reverse=True):
+        try:
+            with open(path) as f:
+                k = json.load(f).get(f"C{cid}", {}).get(kernel)
+        except (OSError, ValueError):
+            continue
+        if k is not None:
+            return int(k["dram_bytes_read"]) + int(k["dram_bytes_write"])
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -242,18 +261,23 @@ def run_ours(args):
     X = make_block(rank, cid)
     sparse = not isinstance(X, np.ndarray)
     m_total = None
+    # sparse configs under torchrun: strong scaling.  Default: the ROW-sharded
+    # layout for n > m (dist_rows.py; each rank keeps its 32-aligned row block,
+    # panels of r x m move); NMFB_DIST_LAYOUT=cols: the column-sharded DistFit
+    rows_layout = sparse and os.environ.get("NMFB_DIST_LAYOUT", "rows") != "cols"
     if sparse:
-        # strong scaling: every rank generates the same config matrix and keeps
-        # its 32-aligned column block of the shard plan
         from paper_1506_08938_b200 import dist as PDm
         from paper_1506_08938_b200.matrix import SparseMatrix
 
         n, m_total = X.rows, X.cols
         xmean = float(X.values.sum()) / (n * m_total)
         xsq_total = float(X.values @ X.values)
-        lo, hi = PDm.ShardPlan(n, m_total, world).col_range(rank)
-        X = PDm.csc_column_block(X, lo, hi) if world > 1 else \
-            SparseMatrix(X.rows, X.cols, X.indptr, X.indices, X.values, validate=False)
+        full = SparseMatrix(X.rows, X.cols, X.indptr, X.indices, X.values, validate=False)
+        if use_dist and not rows_layout:
+            lo, hi = PDm.ShardPlan(n, m_total, world).col_range(rank)
+            X = PDm.csc_column_block(X, lo, hi)
+        else:
+            X = full
         m = X.cols
     else:
         n, m = X.shape
@@ -266,16 +290,26 @@ def run_ours(args):
                     precision="fp32", **knobs)
     mt = m_total if sparse else m * world
     G0, FT0 = initial_factors_from_mean(n, mt, xmean, cfg)
-    if use_dist:
+    if use_dist and rows_layout:
+        from paper_1506_08938_b200.dist_rows import RowShardedFit
+
+        sess = RowShardedFit(X, cfg, init=(G0, FT0))
+        st = sess.state
+        rlo, rhi = sess.plan.row_range(rank)
+        clo, chi = sess.plan.col_range(rank)
+        n_solve, m_solve = rhi - rlo, chi - clo  # this rank's solves
+    elif use_dist:
         from paper_1506_08938_b200 import dist as PD
 
         clo, chi = PD.ShardPlan(n, mt, world).col_range(rank)
         FT0 = FT0[clo:chi]
         sess = PD.DistFit(X, cfg, init=(G0, FT0), m_total=mt)
         st = sess.state
+        n_solve, m_solve = n / world, m
     else:
         sess = FitSession(X, cfg, init=(G0, FT0))
         st = sess.state
+        n_solve, m_solve = n, m
     torch.cuda.synchronize()
 
     def barrier():
@@ -291,10 +325,15 @@ def run_ours(args):
     clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    # timed steps: launch counting, and CUDA events around the dominant
-    # (data-product GEMM) calls only -- the roofline's live launch durations
+    # timed steps: launch counting, and CUDA events around the roofline
+    # kernels' calls only (data products, NNLS) -- their live launch durations
+    # (NNLS too on sparse configs, where it is the dominant kernel; on dense
+    # ones its ~10 us event pairs would be ~3% of a 0.8 ms step, so its
+    # roofline uses the serialised instrumented pass below)
     gemm_names = {"nmfb_tc_gemm", "nmfb_tc_gemm_rows", "nmfb_gemm_tall", "nmfb_csc_linear",
-                  "nmfb_csr_yt_chunked"}
+                  "nmfb_csc_linear_blocked", "nmfb_csr_yt_chunked", "nmfb_csr_yt_chunked_blocked"}
+    if sparse:
+        gemm_names |= {"nmfb_nnls_batch", "nmfb_nnls_batch_peers"}
     with _lib.Recorder(timing=gemm_names) as cnt:
         t0.record()
         for k in range(args.warmup, args.warmup + args.steps):
@@ -304,9 +343,13 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
-    # the same number of steps again with a CUDA event pair around every
-    # C-ABI call: per-kernel durations and shares (the events add small gaps,
-    # so these steps are not the timed ones)
+    # the same number of steps again, SERIALISED (the objective on the main
+    # stream, no side-stream overlap) with a CUDA event pair around every
+    # C-ABI call: per-kernel durations and shares of the step that add up
+    # (these steps are not the timed ones)
+    for obj in (st, getattr(st, "st", None)):
+        if obj is not None:
+            obj.serial = True
     with _lib.Recorder(timing=True) as rec:
         i0 = torch.cuda.Event(enable_timing=True)
         i1 = torch.cuda.Event(enable_timing=True)
@@ -316,6 +359,9 @@ def run_ours(args):
         st.join()
         i1.record()
     torch.cuda.synchronize()
+    for obj in (st, getattr(st, "st", None)):
+        if obj is not None:
+            obj.serial = False
     ms_instr = i0.elapsed_time(i1)
     if use_dist:
         tt = torch.tensor([ms], device="cuda")
@@ -325,9 +371,8 @@ def run_ours(args):
     solves_step = (mt + n)  # per step, all ranks
     value = solves_step * args.steps / (ms / 1e3)
     calls = rec.summary()
-    # dominant kernel: the largest share of the step
-    dom = max(calls.items(), key=lambda kv: kv[1][1])
     hbm, peak_src = peaks()
+    ffma_tf, l2_gbs, micro_src = micro_peaks()
     live = cnt.summary()  # data-product launches inside the timed region
     kernels = {}
     for name, (c, t) in calls.items():
@@ -335,7 +380,7 @@ def run_ours(args):
     share = {k: round(v[1] / ms_instr, 4) for k, v in calls.items()}
     # inner iterations of the timed steps -> k-bar for the NNLS flop count
     inner = st_inner(st, args.warmup, args.warmup + args.steps)
-    kbar = inner / (solves_step * world * args.steps) if inner else 1.0
+    kbar = inner / ((m_solve + n_solve) * args.steps) if inner else 1.0
     rooflines = {}
     if not sparse:
         gname = "nmfb_tc_gemm" if "nmfb_tc_gemm" in calls else "nmfb_gemm_tall"
@@ -343,10 +388,11 @@ def run_ours(args):
         if "nmfb_tc_gemm_rows" in live:  # multi-GPU peer path: X F^T stores into the owners
             c2, t2 = live["nmfb_tc_gemm_rows"]
             gemm_calls, gemm_ms = gemm_calls + c2, gemm_ms + t2
-        # algorithmic bytes per data-product launch, averaged over the two passes
-        # (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once, B^T hi+lo, split-K C
-        se, sm = getattr(st, "splits_e", 1), getattr(st, "splits_m", 1)
-        gemm_bytes = 4.0 * (n * m + R * (n + m) + (se * m + sm * n) * R / 2.0)
+        # algorithmic bytes per data-product launch, averaged over the two
+        # passes (G^T X: A = X^T, K = n; X F^T: A = X, K = m): X once and the
+        # small factor's hi/lo splits (the split-K partial writes are the
+        # kernel's own scratch, not algorithmic)
+        gemm_bytes = 4.0 * (n * m + 2 * R * (n + m) / 2.0)
         gemm_avg_ms = gemm_ms / max(gemm_calls, 1)
         achieved = gemm_bytes / (gemm_avg_ms / 1e3) / 1e9 if gemm_avg_ms > 0 else 0.0
         rooflines["data_products"] = {
@@ -354,42 +400,62 @@ def run_ours(args):
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "peak_source": peak_src,
             "algorithmic_bytes_per_launch": gemm_bytes, "avg_launch_ms": gemm_avg_ms,
-            "timed": "live CUDA events in the timed steps", "traffic": profile_traffic()}
+            "timed": "live CUDA events in the timed steps",
+            "traffic": profile_traffic(cid, gname), "share": share.get(gname)}
     else:
         # compulsory bytes of one SpMM pass: values + indices once,
-        # the pointer array, both factors read/written once
+        # the pointer array, both factors read/written once; the factor-row
+        # gathers (4 nnz r bytes) are served by L2 -> their roof is the
+        # measured L2 read bandwidth
         nnz = X.nnz
+        names = ("nmfb_csc_linear", "nmfb_csc_linear_blocked", "nmfb_csr_yt_chunked",
+                 "nmfb_csr_yt_chunked_blocked")
         sp_bytes = 8.0 * nnz + 8.0 * (m + 1) + 4.0 * (n + m) * R
-        sp_calls = sum(live.get(k, (0, 0.0))[0] for k in ("nmfb_csc_linear", "nmfb_csr_yt_chunked"))
-        sp_ms = sum(live.get(k, (0, 0.0))[1] for k in ("nmfb_csc_linear", "nmfb_csr_yt_chunked"))
+        sp_calls = sum(live.get(k, (0, 0.0))[0] for k in names)
+        sp_ms = sum(live.get(k, (0, 0.0))[1] for k in names)
         sp_avg = sp_ms / max(sp_calls, 1)
         ach = sp_bytes / (sp_avg / 1e3) / 1e9 if sp_avg > 0 else 0.0
+        gbytes = 4.0 * nnz * R
+        gach = gbytes / (sp_avg / 1e3) / 1e9 if sp_avg > 0 else 0.0
         rooflines["data_products"] = {
-            "kernel": "nmfb_csc_linear + nmfb_csr_yt_chunked (G^T X and X F^T, CSC / CSR SpMM)",
-            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-            "peak_source": peak_src, "algorithmic_bytes_per_launch": sp_bytes,
-            "avg_launch_ms": sp_avg, "timed": "live CUDA events in the timed steps",
-            "gather_bytes_per_launch": 4.0 * nnz * R,
-            "gather_achieved_GBps": (4.0 * nnz * R) / (sp_avg / 1e3) / 1e9 if sp_avg > 0 else 0.0,
-            "note": "compulsory bytes; the factor-row gathers (gather_bytes) are served "
-                    "by L2 when the factor fits (C3), by HBM when it does not (C5)"}
-    if "nmfb_nnls_batch" in calls:
-        c, t = calls["nmfb_nnls_batch"]
+            "kernel": "nmfb_csc_linear[_blocked] + nmfb_csr_yt_chunked (G^T X and X F^T, "
+                      "CSC / CSR SpMM with 16-byte factor-row gathers)",
+            "bound": "l2" if l2_gbs else "hbm",
+            "achieved": gach if l2_gbs else ach, "peak": l2_gbs or hbm, "unit": "GB/s",
+            "frac": (gach / l2_gbs) if l2_gbs else ach / hbm,
+            "peak_source": micro_src if l2_gbs else peak_src,
+            "algorithmic_bytes_per_launch": gbytes, "avg_launch_ms": sp_avg,
+            "timed": "live CUDA events in the timed steps",
+            "compulsory_bytes_per_launch": sp_bytes, "compulsory_GBps": ach,
+            "compulsory_frac_of_hbm": ach / hbm, "hbm_peak": hbm,
+            "traffic": profile_traffic(cid, "nmfb_csr_yt_chunked"),
+            "share": round(sum(share.get(k, 0.0) for k in names), 4),
+            "note": "algorithmic bytes = the factor-row gathers (4 nnz r per pass; every "
+                    "nonzero reads its r-row), against the measured L2 read bandwidth"}
+    nn_names = ("nmfb_nnls_batch", "nmfb_nnls_batch_peers")
+    nn_src = live if sparse else calls
+    c = sum(nn_src.get(k, (0, 0.0))[0] for k in nn_names)
+    t = sum(nn_src.get(k, (0, 0.0))[1] for k in nn_names)
+    if c:
         # 2 r^2 (1 + 2 k) flops per solve (gradient init, Q d per
         # inner iteration, r coordinate-descent column updates per iteration)
-        fl = 2.0 * R * R * (1 + 2 * kbar) * (m + n / world)  # this rank's solves
-        nn_ms = t / (c / 2)  # both NNLS launches of one step
+        fl = 2.0 * R * R * (1 + 2 * kbar) * (m_solve + n_solve)  # this rank's solves
+        nn_ms = t / args.steps  # both NNLS launches of one step
         ach = fl / (nn_ms / 1e3) / 1e12
         rooflines["nnls"] = {
             "kernel": "nmfb_nnls_batch (E + M solves of one step)", "bound": "fp32",
-            "achieved": ach, "peak": FP32_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP32_TFLOPS,
-            "peak_source": "spec-derived: 148 SM x 128 FFMA lanes x 2 x measured max SM clock",
-            "algorithmic_flops_per_step": fl, "k_bar": kbar, "ms_per_step": nn_ms,
-            "timed": "instrumented steps (CUDA events around each call)",
-            "note": "counts FMAs only; the greedy-CD argmax scans (r compares per "
-                    "selection) are not counted, so this understates issued work"}
-    dominant_roof = rooflines["data_products"] if not sparse else \
-        max(rooflines.values(), key=lambda rf: rf.get("avg_launch_ms", rf.get("ms_per_step", 0)))
+            "achieved": ach, "peak": ffma_tf, "unit": "TFLOP/s", "frac": ach / ffma_tf,
+            "peak_source": micro_src, "algorithmic_flops_per_step": fl, "k_bar": kbar,
+            "ms_per_step": nn_ms, "avg_launch_ms": nn_ms / 2, "share":
+                round(sum(share.get(k, 0.0) for k in nn_names), 4),
+            "timed": ("live CUDA events in the timed steps" if sparse else
+                      "serialised instrumented steps (CUDA events around each call)"),
+            "traffic": profile_traffic(cid, "nmfb_nnls_batch"),
+            "note": "FMA-counted; the greedy-CD argmax (r compares + a tree per selection) "
+                    "and the shuffles are not counted -- issue-slot utilisation is in "
+                    "profiles/ (ncu smsp__issue_active)"}
+    # the dominant kernel: the largest share of the serialised step
+    dom = max(rooflines.items(), key=lambda kv: kv[1].get("share") or 0.0)
     # log sanity: objective decreasing
     pieces = st.pieces[: args.warmup + args.steps].cpu().numpy()
     xsq = xsq_total if sparse else 0.0
@@ -408,21 +474,25 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "fp32",
         "data": f"synthetic (seeded generator oracle/generators.py, BASELINE C{cid} shape)",
-        "config": {"workload": WORKLOADS[cid], "n": n, "m_per_gpu": m, "rank": R,
-                   "solves_per_step": solves_step,
-                   "step": "one outer iteration of fit(): gram+rescale, G^T X, NNLS(m cols), "
-                           "F F^T, X F^T, NNLS(n rows), objective",
-                   "l2": ("inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
-                          % (n * m * 4 / 1e6)) if not sparse else
-                         ("inputs larger than L2 (CSC + CSR of X = %.0f MB, factors %.0f MB)"
-                          % (16 * X.nnz / 1e6, 4 * (n + m) * R / 1e6)),
-                   "parallelism": f"dp{world} (column-sharded; "
+        "config": config_dict(cid, n, mt),
+        "setup": {"m_per_gpu": m, "solves_per_step": solves_step,
+                  "step": "one outer iteration of fit(): gram+rescale, G^T X, NNLS(m cols), "
+                          "F F^T, X F^T, NNLS(n rows), objective",
+                  "l2": ("inputs larger than L2 (X fp32 = %.0f MB per GPU >> 126 MB)"
+                         % (n * m * 4 / 1e6)) if not sparse else
+                        ("inputs larger than L2 (CSC + CSR of X = %.0f MB, factors %.0f MB)"
+                         % (16 * X.nnz / 1e6, 4 * (n + m) * R / 1e6)),
+                  "parallelism": (f"dp{world} (row-sharded for n > m: row blocks of X and G "
+                                  f"per rank, F replicated; dist_rows.py)" if rows_layout else
+                                  f"dp{world} (column-sharded; "
                                   + ("the config's matrix split across ranks)" if sparse
-                                     else "a config-shaped block per rank)"),
-                   "exchange": ("nvlink peer stores from the producing kernels"
-                                if getattr(sess, "peer", False) else
-                                ("nccl" if use_dist else "none"))},
-        "roofline": dominant_roof,
+                                     else "a config-shaped block per rank)")),
+                  "exchange": ("nvlink peer stores from the producing kernels"
+                               if getattr(sess, "peer", False) else
+                               ("nccl" if use_dist else "none")),
+                  "exchange_bytes_per_rank": (sess.plan.exchange_bytes(R)
+                                              if use_dist and rows_layout else None)},
+        "roofline": dict(dom[1], name=dom[0]),
         "rooflines": rooflines,
         "step_share": share,
         "kernels": kernels,
@@ -434,19 +504,32 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_e2e:
         result["e2e"] = run_e2e(args, X, cfg)
-    if rank == 0 and world == 1 and not args.no_cpu and cid == 2:
-        result["cpu_baseline"] = cpu_baseline(X, bounded=True)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(X, cid)
     if use_dist:
         torch.distributed.destroy_process_group()
     return result if rank == 0 else None
 
 
+def config_dict(cid, n, m):
+    """The `config` of both arms' lines (identical keys, so the driver can
+    pair them)."""
+    from oracle import generators
+
+    c = generators.CONFIGS[cid]
+    return {"workload": WORKLOADS[cid], "config_id": cid, "n": n, "m": m,
+            "rank": c["rank"], "kind": c["kind"]}
+
+
 def run_e2e(args, X, cfg):
-    """Public fit() from host buffers, as a user runs the config: H2D of X
-    (pinned fp32 for dense; the SparseMatrix's CSC arrays for sparse, whose
-    CSR twin is then built on the device), the seeded init, the config's own
-    number of outer iterations (BASELINE.json: C2/C4 100, C3 50, C5 30), D2H
-    of factors and log -- all inside the timed region."""
+    """Public fit() from the reference's own host input type, as a user of the
+    reference calls it: a float64 (n, m) ndarray for dense configs
+    (DenseMatrix's array; the host fp32 cast and the pageable upload are
+    inside the timed region), the float64 / int64 SparseMatrix CSC for sparse
+    ones (upload, index narrowing and the device CSR build inside); seeded
+    init, the config's own number of outer iterations (BASELINE.json: C2/C4
+    100, C3 50, C5 30), D2H of factors and log.  Dense configs also report the
+    pinned fp32 torch-input leg."""
     import torch
 
     from oracle import generators
@@ -456,49 +539,73 @@ def run_e2e(args, X, cfg):
     knobs = config_knobs(args.config)
     R = knobs["rank"]
     K = generators.CONFIGS[args.config]["iters"]
+    ecfg = NmfConfig(max_outer=K, rel_change_tol=0.0, precision="fp32", **knobs)
+    wcfg = NmfConfig(max_outer=2, rel_change_tol=0.0, precision="fp32", **knobs)
+
+    def timed(V):
+        fit(V, wcfg)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        model, log = fit(V, ecfg)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t, log
+
+    out = {}
     if isinstance(X, SparseMatrix):
         n, m = X.rows, X.cols
-        V = X
-        h2d = 8 * (m + 1) + 16 * X.nnz + (n + m) * R * 4
-        call = f"fit(SparseMatrix CSC host arrays, max_outer={K})"
+        h2d = 8 * (m + 1) + 16 * X.nnz
+        dt, log = timed(X)
+        call = f"fit(SparseMatrix float64/int64 CSC host arrays, max_outer={K})"
     else:
         n, m = X.shape
+        h2d = n * m * X.dtype.itemsize  # the float64 bytes cross the link; cast on device
+        dt, log = timed(X)  # the (n, m) float64 array, as DenseMatrix holds it
+        call = f"fit(float64 (n,m) ndarray, max_outer={K})"
         XT = torch.from_numpy(np.ascontiguousarray(X.T, dtype=np.float32)).pin_memory()
-        V = XT.t()  # (n, m) view of the pinned (m, n) buffer
-        h2d = n * m * 4 + (n + m) * R * 4
-        call = f"fit(pinned torch (n,m) fp32 view, max_outer={K})"
-    ecfg = NmfConfig(max_outer=K, rel_change_tol=0.0, precision="fp32", **knobs)
-    fit(V, NmfConfig(max_outer=2, rel_change_tol=0.0, precision="fp32", **knobs))
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    model, log = fit(V, ecfg)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t
+        dt_p, _ = timed(XT.t())
+        out["pinned_fp32_leg"] = {"value": (n + m) * K / dt_p, "unit": "solves/s",
+                                  "seconds": dt_p,
+                                  "call": f"fit(pinned torch (n,m) fp32 view, max_outer={K})"}
     d2h = (n + m) * R * 8 + K * (12 * 8 + 4 * 8)
-    return {"value": (n + m) * K / dt, "unit": "solves/s",
-            "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-            "steps": K, "seconds": dt, "call": call, "final_objective": log.final_objective}
+    out.update({"value": (n + m) * K / dt, "unit": "solves/s",
+                "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+                "steps": K, "seconds": dt, "call": call,
+                "final_objective": log.final_objective})
+    return out
 
 
 # ---------------------------------------------------------------------------
 # reference arm / cpu baseline: the oracle port on this host's cores
 # ---------------------------------------------------------------------------
-def cpu_baseline(X, bounded=True, iters=1):
+def cpu_baseline(X, cid):
+    """The oracle port (bit-exact restatement of the reference: C kernels +
+    numpy/OpenBLAS, one shard worker per host core) on a bounded sample of
+    the same workload: CPU_SAMPLE_ITERS[cid] outer iterations of the full
+    config matrix from the seeded init."""
     from oracle import nmf_oracle as orc
+    from paper_1506_08938_b200.matrix import SparseMatrix
 
     cores = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    n, m = X.shape
-    cfg = orc.Config(rank=RANK, max_outer=iters, seed=SEED, rel_change_tol=0.0, workers=cores)
-    orc.fit(X[:64, :64], orc.Config(rank=4, max_outer=1, seed=0))  # load the C library
+    sparse = isinstance(X, SparseMatrix)
+    if sparse:
+        Xo = orc.Csc(X.rows, X.cols, X.indptr, X.indices, X.values)
+        n, m = X.rows, X.cols
+    else:
+        Xo = X
+        n, m = X.shape
+    iters = CPU_SAMPLE_ITERS[cid]
+    knobs = config_knobs(cid)
+    cfg = orc.Config(max_outer=iters, rel_change_tol=0.0, workers=cores, **knobs)
+    orc.fit(np.ones((64, 64)), orc.Config(rank=4, max_outer=1, seed=0))  # load the C library
     timer = {}
     t = time.perf_counter()
-    G, FT, log = orc.fit(X, cfg, step_timer=timer)
+    orc.fit(Xo, cfg, step_timer=timer, chunked_objective=sparse)
     dt = time.perf_counter() - t
     return {"value": (n + m) * iters / dt, "unit": "solves/s", "cores": cores, "kind": "port",
-            "sample": f"{iters} outer iteration(s) of the full C2 workload (10000x20000, r=50) "
-                      f"in float64 by the oracle port (C kernels + numpy/OpenBLAS, "
-                      f"{cores} shard threads), objective included",
+            "sample": f"{iters} outer iteration(s) of the full C{cid} workload ({n}x{m}, "
+                      f"r={knobs['rank']}) in float64 by the oracle port (C kernels + "
+                      f"numpy/OpenBLAS, {cores} shard threads), objective included",
             "seconds": dt, "em_only_solves_per_s": (n + m) * iters / timer["em_seconds"]}
 
 
@@ -508,8 +615,8 @@ def run_reference(args):
     cores) on this arm's config; one step = one outer iteration, the state
     carried between steps.  Sparse configs use the port's threaded C nnz loop
     for the objective's cross term (same formula, matrix.py:240-253) and, at
-    config 5 (~30 s per iteration), run at most 2 timed steps after no warm-up
-    so the run stays within minutes."""
+    config 5 (~22 s per iteration on 16 threads), run at most 2 timed steps
+    after no warm-up so the run stays within minutes."""
     world, rank, _ = dist_env()
     if rank != 0:
         return None
@@ -524,6 +631,8 @@ def run_reference(args):
     steps, warmup = args.steps, args.warmup
     if cid == 5:
         steps, warmup = min(steps, 2), 0
+    elif cid in (2, 4):
+        steps, warmup = min(steps, 5), min(warmup, 1)
     cfg = orc.Config(max_outer=1, rel_change_tol=0.0, workers=cores, **knobs)
     orc.fit(np.ones((64, 64)), orc.Config(rank=4, max_outer=1, seed=0))  # load the C library
     G, FT = orc.initial_factors(X, cfg)
@@ -534,13 +643,14 @@ def run_reference(args):
         times.append(time.perf_counter() - t)
     dt = sum(times[warmup:])
     value = (n + m) * steps / dt
+    mt = m * world if not sparse else m
     return {"impl": "reference", "metric": "column NNLS solves/sec (NMF outer iteration: "
             "E+M steps + objective)", "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": steps, "warmup": warmup, "ms_per_step": dt / steps * 1e3,
             "higher_is_better": True, "scaling": "strong" if sparse else "weak",
             "vs_baseline": None, "dtype": "fp64",
             "data": "synthetic (same generator as our arm)",
-            "config": {"workload": WORKLOADS[cid], "n": n, "m": m, "rank": knobs["rank"]},
+            "config": config_dict(cid, n, mt),
             "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
                              "sample": f"{steps} outer iterations of C{cid} (after {warmup} "
                                        f"warm-up), oracle port, {cores} threads"},

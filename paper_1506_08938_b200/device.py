@@ -146,6 +146,54 @@ def device_sum_squares(x):
 # ---------------------------------------------------------------------------
 # data matrix on the device
 # ---------------------------------------------------------------------------
+_STAGE = {}  # (dtype, rows, cols) -> two pinned staging buffers, reused across fits
+
+
+def upload_host(arr, dt, device, chunk_bytes=128 << 20, threads=8):
+    """A C-contiguous 2-D host array -> a device tensor of dtype dt.  The
+    rows stream through two pinned staging buffers: host threads copy chunk
+    i + 1 (numpy releases the GIL) while chunk i uploads, and the dtype cast
+    (e.g. the reference's float64 -> fp32) runs on the device -- no host-side
+    astype of the whole matrix, no pageable copy."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rows, cols = arr.shape
+    out = torch.empty((rows, cols), dtype=dt, device=device)
+    if arr.size == 0:
+        return out
+    src_t = torch.from_numpy(arr[:1]).dtype
+    rb = max(1, chunk_bytes // max(1, cols * arr.itemsize))
+    key = (src_t, rb, cols)
+    stage = _STAGE.get(key)
+    if stage is None:
+        _STAGE.clear()  # one staging pair at a time (pinned host memory is precious)
+        stage = _STAGE[key] = [torch.empty((rb, cols), dtype=src_t).pin_memory()
+                               for _ in range(2)]
+    done = [None, None]
+    stream = torch.cuda.current_stream(device)
+
+    def fill(buf, lo, hi, pool):
+        dst = buf.numpy()[: hi - lo]
+        parts = threads
+        step = -(-(hi - lo) // parts)
+        list(pool.map(lambda q: np.copyto(dst[q * step:(q + 1) * step],
+                                          arr[lo + q * step: min(hi, lo + (q + 1) * step)]),
+                      range(parts)))
+
+    with ThreadPoolExecutor(threads) as pool:
+        for i, lo in enumerate(range(0, rows, rb)):
+            hi = min(rows, lo + rb)
+            b = i % 2
+            if done[b] is not None:
+                done[b].synchronize()  # the upload that last used this buffer
+            fill(stage[b], lo, hi, pool)
+            out[lo:hi].copy_(stage[b][: hi - lo], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done[b] = ev
+    return out
+
+
 class DeviceData:
     """X on the device.  Dense: XT (m, n) row-major == the reference's
     Fortran-ordered (n, m) buffer.  Sparse: CSC (int64 indptr, int32 rows,
@@ -203,13 +251,18 @@ class DeviceData:
                 raise ValueError("dense data must be 2-D")
             self.kind = "dense"
             self.n, self.m = arr.shape
-            xt = np.ascontiguousarray(arr.T)  # no copy for Fortran input
-            if dt == torch.float32 and xt.dtype != np.float32:
-                xt = xt.astype(np.float32)
-            elif dt == torch.float64 and xt.dtype != np.float64:
-                xt = xt.astype(np.float64)
-            self.XT = torch.from_numpy(xt).to(self.device)
             self.host = None
+            if (arr.flags["C_CONTIGUOUS"] and not arr.flags["F_CONTIGUOUS"]
+                    and dt == torch.float32):
+                # (n, m) row-major host data: uploaded as X and transposed on
+                # the device (no host transpose of the whole matrix)
+                self.X = upload_host(arr, dt, self.device)
+                self.XT = torch.empty((self.m, self.n), dtype=dt, device=self.device)
+                L.call("nmfb_transpose", vp(self.X), self.n, self.m, vp(self.XT),
+                       stream_handle())
+            else:
+                # the reference's Fortran-ordered buffer == XT row-major
+                self.XT = upload_host(np.ascontiguousarray(arr.T), dt, self.device)
 
     def spmm_blocking(self, r):
         """L2 blocking plan of the sparse data products for rank r (fp32):
@@ -558,20 +611,22 @@ class Alternation:
                 L.call("nmfb_slice_u8", vp(self.FT), self.m, self.r, self.r, vp(self.Fsl[q]),
                        self._st())
             # the residual runs on a side stream, overlapping the next iteration
+            # (serial=True, for per-kernel timing: on the caller's stream)
             ready = torch.cuda.Event()
             ready.record()
-            self.side.wait_event(ready)
-            with torch.cuda.stream(self.side):
+            side = torch.cuda.current_stream() if getattr(self, "serial", False) else self.side
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
                 if self.use_i8:
                     L.call("nmfb_residual_i8", vp(d.X), self.n, self.m, vp(self.Gsl[q]),
                            vp(self.Fsl[q]), self.r, vp(p[0:1]), vp(self.rq_ws),
-                           stream_handle(self.side))
+                           stream_handle(side))
                 else:
                     L.call("nmfb_dense_residual_kmajor", vp(d.XT), self.m, self.n, vp(Gt[0]),
                            vp(Ft[0]), self.r, vp(p[0:1]), vp(self.res_ws),
-                           stream_handle(self.side))
+                           stream_handle(side))
                 ev = torch.cuda.Event()
-                ev.record(self.side)
+                ev.record(side)
             self.res_ev[q] = ev
         elif d.kind == "dense":
             # 0.5 ||X - G F||^2 by tile residual; G F never stored

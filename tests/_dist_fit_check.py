@@ -26,7 +26,7 @@ def main(out_path):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rng = np.random.default_rng(3)
     K = 6
-    if os.environ.get("NMFB_CHECK_SPARSE") == "1":
+    if os.environ.get("NMFB_CHECK_SPARSE") == "1" or os.environ.get("NMFB_CHECK_ROWS") == "1":
         # sparse column block through DistFit(m_total=...) (the config 3/5
         # strong-scaling path of bench.py)
         from oracle import generators
@@ -51,7 +51,13 @@ def main(out_path):
         single.iterate(k)
     single.join()
 
-    sess = PD.DistFit(block, cfg, init=(G0, FT0), m_total=m)
+    if os.environ.get("NMFB_CHECK_ROWS") == "1":
+        # the row-sharded layout for tall sparse data (dist_rows.py)
+        from paper_1506_08938_b200.dist_rows import RowShardedFit
+
+        sess = RowShardedFit(X, cfg, init=(G0, FT0))
+    else:
+        sess = PD.DistFit(block, cfg, init=(G0, FT0), m_total=m)
     st = sess.state
     for k in range(K):
         st.iterate(k)

@@ -1,27 +1,26 @@
 """Parity at the BASELINE.json configs' FULL sizes (C2-C5), fp32 production path.
 
-The oracle cannot run the full trajectories at these sizes in test time
-(C2 is ~2.4 s per iteration with 16 threads, C5 ~70 s), so each
-config is checked through properties that do not depend on size:
+Per config (SURVEY.md 7.3 P2/P3 at full size):
 
-* teacher-forced subproblems on sampled fast-break blocks: G and F are read
-  back before and after one GPU outer iteration; for 8 seeded 32-aligned
-  blocks of columns (E-step) and rows (M-step) the oracle (the bit-exact C
-  restatement of kernels.py) rebuilds the problems in float64 from the same
-  G_k / F_{k+1} -- Q = Gram + 2 lambda I (parallel.py:104,196), h = mu1 - G^T x_j
-  (kernels.py:251-258,306-313) / beta1 - (X F^T)_i (kernels.py:361) -- and
-  solves them with the reference's stopping rule and fast-break blocks.
-  Blocks are 32-aligned, so the reference's per-block threshold resets
-  (kernels.py:246-248) make a sampled block exactly the reference's problem
-  sequence.  fp32 tolerance: 1e-5 on the summed subproblem objective, and the
-  factors within 10x of the oracle's own movement when only its inputs are
-  rounded to float32 (the problems' conditioning, not the kernels, sets the
-  factor-level agreement an fp32 path can reach at these sizes);
-* the device objective equals a host float64 evaluation of the same factors
-  (dense: chunked 0.5 ||X - GF||^2 plus the penalties, nmf.py:152-165; sparse:
-  matrix.py:240-253, the cross term as a threaded C nnz loop);
-* the objective is non-increasing (block coordinate descent), the factors are
-  finite and nonnegative, and at C4 the L1 penalty leaves exact zeros in H.
+* free-running trajectory: the fp32 GPU fit and the fp64 oracle (the
+  bit-exact port of the reference) run K outer iterations from the same
+  seeded init; the oracle also runs on the fp32-ROUNDED input -- the
+  storage-rounding envelope every fp32 implementation starts from (the
+  reference itself moves that much).  Asserted per iteration:
+  objective within the north-star 1e-4, or within 10x of that envelope where
+  the envelope itself exceeds 1e-4 (the dense configs' early iterations);
+* the device objective equals a host float64 evaluation of the returned
+  factors (dense: chunked 0.5 ||X - GF||^2 plus penalties, nmf.py:152-165;
+  sparse: matrix.py:240-253 with a threaded C nnz loop for the cross term);
+* sampled subproblems of the last iteration (8 seeded 32-aligned blocks of
+  columns and of rows, rebuilt in float64 from the GPU's own G_k / F_{k+1}):
+  the fp32 production NNLS kernel against the fp64 check-mode kernel (== the
+  reference's solver, bit for bit) on IDENTICAL fp32-rounded inputs -- the
+  arithmetic-only error.  Reported: decision flips (a problem whose inner
+  iteration count or zero pattern differs), the factor error of the
+  problems without a flip, the summed subproblem objective gap;
+* the objective is non-increasing, factors finite and nonnegative, and at C4
+  the L1 penalty leaves exact zeros in H.
 """
 
 import os
@@ -60,32 +59,39 @@ def _phi(H, h, x):
 
 
 def _compare(tag, H, h, warm, x_gpu, cfg):
-    """GPU solutions vs the oracle's on the same float64 problems.
-
-    The summed subproblem objective must agree to 1e-5 (north star: 1e-4 on
-    the objective).  Factor-level agreement is bounded by the problems'
-    conditioning: the oracle's own solutions move when only its inputs are
-    rounded to float32 (Q and h, as the GPU holds them), so the GPU's factor
-    error must lie within 10x of that float32-input sensitivity."""
-    from gpu_util import floored_rel
+    """Sampled subproblems: (1) the production output against the oracle on
+    the float64 problems (summed subproblem objective); (2) the fp32
+    production kernel against the fp64 check-mode kernel on identical
+    fp32-rounded inputs: decision flips and the factor error without one."""
+    from gpu_util import floored_rel, nnls
 
     def per(a, b):
         return np.array([floored_rel(u[None], v[None]) for u, v in zip(a, b)])
 
     xo = _solve_blocks(H, h, warm, cfg)
-    H32 = H.astype(np.float32).astype(np.float64)
-    h32 = h.astype(np.float32).astype(np.float64)
-    xo32 = _solve_blocks(H32, h32, warm.astype(np.float32).astype(np.float64), cfg)
-    e_gpu, e_sens = per(x_gpu, xo), per(xo32, xo)
     pg, po = _phi(H, h, x_gpu), _phi(H, h, xo)
     gap = abs(pg.sum() - po.sum()) / abs(po.sum())
-    q = lambda e, p: float(np.percentile(e, p))  # noqa: E731
-    print(f"{tag}: factor rel GPU vs oracle median {q(e_gpu, 50):.2e} p90 {q(e_gpu, 90):.2e}; "
-          f"oracle fp32-input sensitivity median {q(e_sens, 50):.2e} p90 {q(e_sens, 90):.2e}; "
-          f"within 1e-3 {float((e_gpu < 1e-3).mean()):.3f}; summed objective gap {gap:.2e}")
+    r32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
+    H32, h32, w32 = r32(H), r32(h), r32(warm)
+    x64, it64, _, _ = nnls(H32, h32, w32, cfg["epsilon"], cfg["inner_cap"], precision="fp64")
+    x32, it32, _, _ = nnls(H32, h32, w32, cfg["epsilon"], cfg["inner_cap"], precision="fp32")
+    flip = (it64 != it32) | np.any((x64 == 0) != (x32 == 0), axis=1)
+    e = per(x32, x64)
+    keep = ~flip
+    q = lambda v, p: float(np.percentile(v, p)) if len(v) else 0.0  # noqa: E731
+    g32 = abs(_phi(H32, h32, x32).sum() - _phi(H32, h32, x64).sum()) / abs(_phi(H32, h32, x64).sum())
+    print(f"{tag}: {len(e)} problems, decision flips {int(flip.sum())} "
+          f"({float(flip.mean()):.3f}); factor err without a flip median {q(e[keep], 50):.1e} "
+          f"p90 {q(e[keep], 90):.1e} max {q(e[keep], 100):.1e}; with flips median "
+          f"{q(e[flip], 50):.1e}; kernel objective gap {g32:.1e}; production vs oracle "
+          f"summed objective gap {gap:.2e}")
     assert gap < 1e-5, (tag, gap)
-    assert q(e_gpu, 50) <= max(10 * q(e_sens, 50), 1e-5), tag
-    assert q(e_gpu, 90) <= max(10 * q(e_sens, 90), 1e-4), tag
+    assert g32 < 1e-5, (tag, g32)
+    # arithmetic-only error where the solver takes the reference's decisions
+    assert q(e[keep], 50) < 1e-4, tag
+    assert q(e[keep], 90) < 1e-3, tag
+    return dict(problems=len(e), flips=int(flip.sum()), err_noflip_median=q(e[keep], 50),
+                err_noflip_p90=q(e[keep], 90), kernel_gap=g32, gap=gap)
 
 
 def _dense_objective(x, G, F):
@@ -132,6 +138,21 @@ def test_full_size_config(cid):
     G = st.G.double().cpu().numpy()
     FT = st.FT.double().cpu().numpy()
     print(f"C{cid}: objectives {objs}")
+    # free-running trajectory vs the oracle and its fp32-input envelope
+    oc = orc.Config(workers=os.cpu_count() or 1, **kw)
+    G0, FT0 = orc.initial_factors(x, oc)
+    _, _, olog = orc.fit(x, oc, chunked_objective=sparse)
+    xr = orc.Csc(x.rows, x.cols, x.indptr, x.indices, x.values.astype(np.float32).astype(
+        np.float64)) if sparse else x.astype(np.float32).astype(np.float64)
+    _, _, rlog = orc.fit(xr, oc, chunked_objective=sparse)
+    o, fl = np.asarray(olog.objective), np.asarray(rlog.objective)
+    rel = np.abs(np.asarray(objs) - o) / o
+    env = np.abs(fl - o) / o
+    print(f"C{cid}: trajectory rel err {['%.1e' % v for v in rel]}, fp32-input envelope "
+          f"{['%.1e' % v for v in env]}")
+    assert np.all(rel <= np.maximum(1e-4, 10.0 * env.max())), (rel, env)
+    if sparse:
+        assert rel.max() < 1e-4, rel
     assert np.isfinite(G).all() and np.isfinite(FT).all()
     assert (G >= 0).all() and (FT >= 0).all()
     assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:])), objs

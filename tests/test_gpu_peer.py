@@ -245,3 +245,11 @@ def test_dist_world1_sparse_block_equals_single_gpu(tmp_path):
     path): bit-identical to the single-GPU fit."""
     res = _torchrun({"NMFB_CHECK_SPARSE": "1", "NMFB_DIST_PEER": "0"}, tmp_path, "sparse")
     assert res["G_equal"] and res["FT_equal"] and res["obj_equal"], res
+
+
+def test_dist_world1_row_sharded_sparse_equals_single_gpu(tmp_path):
+    """torchrun, one rank, the ROW-sharded layout for tall sparse data
+    (dist_rows.py: Gram / H_f allreduces, reduce-scatter of the partial linear
+    terms, allgather of F over NCCL): bit-identical to the single-GPU fit."""
+    res = _torchrun({"NMFB_CHECK_ROWS": "1"}, tmp_path, "rows")
+    assert res["G_equal"] and res["FT_equal"] and res["obj_equal"], res

@@ -56,6 +56,10 @@ def gpu_step(V, gcfg, G, FT, mode):
     d = D.DeviceData(V, "fp32")
     st = D.Alternation(d, gcfg, G, FT, 1, precision="fp32", kernel_mode=L.MODE_REFERENCE)
     st.iterate(0)
+    st.join()
+    import torch
+
+    torch.cuda.synchronize()
     xsq = 0.0 if isinstance(V, np.ndarray) else float(np.asarray(V.values, np.float32).astype(np.float64) @ np.asarray(V.values, np.float32).astype(np.float64))
     return st.assemble(st.pieces[0].cpu().numpy(), gcfg, d.kind, xsq)
 
