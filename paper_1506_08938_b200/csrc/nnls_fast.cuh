@@ -217,7 +217,12 @@ __device__ __forceinline__ float fast_h(const NnlsArgs<float, TH> &a, int64_t j,
 
 // Occupancy target: ~4E + 48 live registers per thread (y, grad and Q*d per
 // coordinate; the passive gradient and step are recomputed) -> CTAs per SM.
-__host__ __device__ constexpr int nnls_regs(int E, int L) { return 4 * E + 48 + (L == 1 ? 48 : 0); }
+#ifndef NMFB_NNLS_REG_SLACK
+#define NMFB_NNLS_REG_SLACK 0
+#endif
+__host__ __device__ constexpr int nnls_regs(int E, int L) {
+    return 4 * E + 48 + (L == 1 ? 48 : 0) + NMFB_NNLS_REG_SLACK;
+}
 __host__ __device__ constexpr int nnls_min_blocks(int E, int L, int threads) {
     return (65536 / (nnls_regs(E, L) * threads)) < 1 ? 1 : (65536 / (nnls_regs(E, L) * threads));
 }
@@ -240,7 +245,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     __shared__ float blk_norm[B][32], blk_final[B][32];
     __shared__ int blk_status[B][32];
     __shared__ int blk_any[B];
-    __shared__ int act_s[R];      // act_idx / scale_a staged once per CTA
+    __shared__ int act_s[R];      // act_idx / scale_a / active staged once per CTA
+    __shared__ unsigned char actv_s[R];
     __shared__ float scl_s[R];
 
     const int tid = threadIdx.x;
@@ -269,6 +275,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
             act_s[k] = a.act_idx[k];
             scl_s[k] = a.scale_a[k];
         }
+        for (int i = tid; i < r; i += blockDim.x) actv_s[i] = a.active[i];
     }
     __syncthreads();
 
@@ -329,6 +336,16 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         // act_idx the identity) exactly the compact layout; otherwise
         // h[act_idx[k]] is gathered again (an L1/L2 hit).
         float hreg[STAGE_H ? 1 : EE];
+        // the warm-start row is independent of h: its loads go out first
+        // (with every dimension active, lane l reads x[j][e*L + l])
+        float xw[STAGE_H ? 1 : EE];
+        if constexpr (!STAGE_H) {
+#pragma unroll
+            for (int e = 0; e < EE; ++e) {
+                const int k = e * L + l;
+                xw[e] = (valid && k < ra) ? a.x[j * r + (ra == r ? k : act_s[k])] : 0.f;
+            }
+        }
         float *hrow = smem_f + R * SP + (size_t)slot * r;
         bool any_neg = false, frozen_neg = false;
         if constexpr (STAGE_H) {
@@ -338,23 +355,24 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                     hrow[i] = hv;
                     if (hv < 0.f) {
                         any_neg = true;
-                        if (!a.active[i]) frozen_neg = true;
+                        if (!actv_s[i]) frozen_neg = true;
                     }
                 }
             }
             __syncwarp(gmask);
         } else {
+            // all loads first (independent, in flight together), then the checks
 #pragma unroll
             for (int e = 0; e < EE; ++e) {
                 const int i = e * L + l;
-                hreg[e] = 0.f;
-                if (valid && i < r) {
-                    const float hv = fast_h<TH>(a, j, i);
-                    hreg[e] = hv;
-                    if (hv < 0.f) {
-                        any_neg = true;
-                        if (!a.active[i]) frozen_neg = true;
-                    }
+                hreg[e] = (valid && i < r) ? fast_h<TH>(a, j, i) : 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < EE; ++e) {
+                const int i = e * L + l;
+                if (hreg[e] < 0.f) {
+                    any_neg = true;
+                    if (i < r && !actv_s[i]) frozen_neg = true;
                 }
             }
         }
@@ -382,7 +400,10 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                 else
                     hv = ident ? hreg[e] : fast_h<TH>(a, j, ik);
                 qv = __fdiv_rn(hv, sv);
-                yv = a.x[j * r + ik] * sv;
+                if constexpr (STAGE_H)
+                    yv = a.x[j * r + ik] * sv;
+                else
+                    yv = xw[e] * sv;
             }
             y[e] = yv;
             gr[e] = qv;

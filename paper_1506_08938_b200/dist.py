@@ -483,7 +483,9 @@ def peer_agreed(engine, group=None):
     ok = peer_wanted(engine)
     if ok:
         try:  # local prerequisites, checked before the collective decision
-            import torch.distributed._symmetric_memory  # noqa: F401
+            import importlib
+
+            importlib.import_module("torch.distributed._symmetric_memory")
         except Exception:
             ok = False
     P = int(getattr(engine.st, "splits_m", 0)) if ok else 0
