@@ -234,7 +234,8 @@ int nmfb_csr_yt(int dtype, int mode, const int64_t *rowptr, const int32_t *colid
  * paper_1506_08938_b200/device.py csr_chunk_plan).  chunks: int64
  * [nchunks][4] = (row, lo, hi, slot) with slot -1 for single-chunk rows;
  * heavy: int64 [nheavy][3] = (row, first slot, count); part: workspace of
- * (total slots) x r elements of yt_dtype.  Deterministic. */
+ * (total slots) x r doubles (the fp32 production form accumulates every row
+ * in fp64 and rounds Y^T once; yt_dtype is the output type).  Deterministic. */
 int nmfb_csr_yt_chunked(int dtype, const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
                         int64_t nheavy, const int32_t *colidx, const void *vals, const void *FT,
                         int32_t r, int yt_dtype, void *YT, void *part, void *stream);

@@ -205,12 +205,14 @@ __device__ __forceinline__ float fast_h(const NnlsArgs<float, TH> &a, int64_t j,
     if (a.S == 0) return (float)p[0];
     TH s0 = p[0], s1 = TH(0), s2 = TH(0), s3 = TH(0);
     int k = 1;
+#pragma unroll 1
     for (; k + 3 < a.S; k += 4) {
         s0 += p[(int64_t)k * a.h_pstride];
         s1 += p[(int64_t)(k + 1) * a.h_pstride];
         s2 += p[(int64_t)(k + 2) * a.h_pstride];
         s3 += p[(int64_t)(k + 3) * a.h_pstride];
     }
+#pragma unroll 1
     for (; k < a.S; ++k) s0 += p[(int64_t)k * a.h_pstride];
     return (float)((TH)a.h_base - ((s0 + s1) + (s2 + s3)));
 }
@@ -303,8 +305,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         const float *Qsl = Qs + l * LS;  // this lane's block of every row
         // the warp's q_times_w4 exchange buffer (128 floats) and, in the CD
         // phase, this problem's y row (lane l's coordinates at l*LS + e)
-        float *wscr = smem_f + R * SP + (size_t)warp * 128;
-        float *ys = smem_f + R * SP + (STAGE_H ? (size_t)32 * B * r : (size_t)128 * L * B) +
+        float *wscr = smem_f + R * SP + (size_t)32 * B * r + (size_t)warp * 128;
+        float *ys = smem_f + R * SP + (size_t)32 * B * r + (STAGE_H ? 0 : (size_t)128 * L * B) +
                     (size_t)slot * SP + l * LS;
         // q_times source-lane rotation: one offset per quarter-warp (see q_times_f)
         // (measured: pays at E = 25, costs at E <= 13, where the per-lane source
@@ -328,54 +330,45 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
         float final_norm = 0.f, norm_k = 0.f, threshold = 0.f;
 
         // ---- prologue: short-circuit, frozen check, compact load, gradient ----
-        // The problem's full linear term h (sum of the split-K partials, loads
-        // issued 4 at a time) is scanned for the short-circuit / frozen checks.
-        // Small E (STAGE_H): staged once in a shared-memory row that the
-        // compact gather h[act_idx[k]] reads back.  Large E: lane l holds
-        // h[e*L + l] in registers -- with every dimension active (ra == r,
-        // act_idx the identity) exactly the compact layout; otherwise
-        // h[act_idx[k]] is gathered again (an L1/L2 hit).
-        float hreg[STAGE_H ? 1 : EE];
-        // the warm-start row is independent of h: its loads go out first
-        // (with every dimension active, lane l reads x[j][e*L + l])
-        float xw[STAGE_H ? 1 : EE];
-        if constexpr (!STAGE_H) {
+        // The warm-start row is independent of h: its loads go out first (with
+        // every dimension active lane l reads x[j][e*L + l]).  The problem's
+        // full linear term h (sum of the split-K partials) is staged in its
+        // shared-memory row, four rows' loads in flight per lane -- a compact
+        // loop, not E inlined copies of the partial sums (the prologue code
+        // would otherwise crowd the CD loop out of the instruction cache) --
+        // and scanned for the short-circuit / frozen checks; the compact gather
+        // h[act_idx[k]] reads it back.
+        float xw[EE];
 #pragma unroll
-            for (int e = 0; e < EE; ++e) {
-                const int k = e * L + l;
-                xw[e] = (valid && k < ra) ? a.x[j * r + (ra == r ? k : act_s[k])] : 0.f;
-            }
+        for (int e = 0; e < EE; ++e) {
+            const int k = e * L + l;
+            xw[e] = (valid && k < ra) ? a.x[j * r + (ra == r ? k : act_s[k])] : 0.f;
         }
         float *hrow = smem_f + R * SP + (size_t)slot * r;
         bool any_neg = false, frozen_neg = false;
-        if constexpr (STAGE_H) {
-            if (valid) {
-                for (int i = l; i < r; i += L) {
-                    const float hv = fast_h<TH>(a, j, i);
-                    hrow[i] = hv;
-                    if (hv < 0.f) {
-                        any_neg = true;
-                        if (!actv_s[i]) frozen_neg = true;
+        if (valid) {
+#pragma unroll 1
+            for (int i0 = l; i0 < r; i0 += 4 * L) {
+                float hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * L;
+                    hv[u] = (i < r) ? fast_h<TH>(a, j, i) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + u * L;
+                    if (i < r) {
+                        hrow[i] = hv[u];
+                        if (hv[u] < 0.f) {
+                            any_neg = true;
+                            if (!actv_s[i]) frozen_neg = true;
+                        }
                     }
                 }
             }
-            __syncwarp(gmask);
-        } else {
-            // all loads first (independent, in flight together), then the checks
-#pragma unroll
-            for (int e = 0; e < EE; ++e) {
-                const int i = e * L + l;
-                hreg[e] = (valid && i < r) ? fast_h<TH>(a, j, i) : 0.f;
-            }
-#pragma unroll
-            for (int e = 0; e < EE; ++e) {
-                const int i = e * L + l;
-                if (hreg[e] < 0.f) {
-                    any_neg = true;
-                    if (i < r && !actv_s[i]) frozen_neg = true;
-                }
-            }
         }
+        __syncwarp(gmask);
         any_neg = gany<L>(any_neg, gmask, gbase);
         frozen_neg = gany<L>(frozen_neg, gmask, gbase);
         if (valid) {
@@ -394,16 +387,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
             if (solve && k < ra) {
                 const int ik = ident ? k : act_s[k];
                 const float sv = scl_s[k];
-                float hv;
-                if constexpr (STAGE_H)
-                    hv = hrow[ik];
-                else
-                    hv = ident ? hreg[e] : fast_h<TH>(a, j, ik);
-                qv = __fdiv_rn(hv, sv);
-                if constexpr (STAGE_H)
-                    yv = a.x[j * r + ik] * sv;
-                else
-                    yv = xw[e] * sv;
+                qv = __fdiv_rn(hrow[ik], sv);
+                yv = xw[e] * sv;
             }
             y[e] = yv;
             gr[e] = qv;
@@ -834,13 +819,13 @@ template <typename TH, int E, int L, int B>
 static int launch_fast_variant(const NnlsLaunch &p) {
     auto a = make_args<float, TH>(p);
     constexpr int R = E * L, SP = L * nnls_ls(E);
-    // Q (R x SP, permuted rows) + small E: one staged h row (r floats) per
-    // problem slot; large E: a 128-float q_times_w4 exchange buffer per warp;
-    // + one y row (SP floats) per problem slot for the greedy CD
+    // Q (R x SP, permuted rows) + one staged h row (r floats) per problem
+    // slot + large E: a 128-float q_times_w4 exchange buffer per warp
+    // (+ the YSMEM experiment's y rows)
     constexpr bool STAGE_H = E < NMFB_NNLS_W4_MIN_E;
     constexpr bool YSMEM = NMFB_NNLS_EXACT_ARGMAX && NMFB_NNLS_YSMEM;
-    size_t smem = sizeof(float) * ((size_t)R * SP + (STAGE_H ? (size_t)32 * B * p.r
-                                                              : (size_t)128 * L * B) +
+    size_t smem = sizeof(float) * ((size_t)R * SP + (size_t)32 * B * p.r +
+                                   (STAGE_H ? 0 : (size_t)128 * L * B) +
                                    (YSMEM ? (size_t)32 * B * SP : 0));
 
     auto kern = nnls_fast_kernel<TH, E, L, B, false>;

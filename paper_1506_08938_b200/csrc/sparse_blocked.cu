@@ -103,11 +103,13 @@ __global__ void __launch_bounds__(128) csc_linear_v4x_kernel(
     }
 }
 
-template <typename TY, int NV>
+// TA: accumulation type (the heavy-row chunk partials too), TY: the Y^T
+// output (fp32 Y^T is accumulated in fp64 and rounded once)
+template <typename TA, typename TY, int NV>
 __global__ void __launch_bounds__(128) csr_yt_chunk_v4x_kernel(
     const int64_t *__restrict__ chunks, int64_t nchunks, const int64_t *__restrict__ seg, int nblk,
     int b, const int32_t *__restrict__ colidx, const float *__restrict__ vals,
-    const float *__restrict__ FT, int r, TY *__restrict__ YT, TY *__restrict__ part) {
+    const float *__restrict__ FT, int r, TY *__restrict__ YT, TA *__restrict__ part) {
     const int64_t ch = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (ch >= nchunks) return;
     const int lane = threadIdx.x & 31;
@@ -119,13 +121,16 @@ __global__ void __launch_bounds__(128) csr_yt_chunk_v4x_kernel(
         p0 = seg[ch * (nblk + 1) + b];
         p1 = seg[ch * (nblk + 1) + b + 1];
     }
-    TY *out = (slot < 0) ? (YT + row * r) : (part + slot * r);
-    TY a[NV][4];
+    TY *outy = YT + row * r;
+    TA *outp = part + slot * r;
+    TA a[NV][4];
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
         const int c = lane + 32 * q;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) a[q][t] = (b > 0 && c < nq) ? out[4 * c + t] : TY(0);
+        for (int t = 0; t < 4; ++t)
+            a[q][t] = (b > 0 && c < nq) ? (slot < 0 ? (TA)outy[4 * c + t] : outp[4 * c + t])
+                                        : TA(0);
     }
     for (int64_t base = p0; base < p1; base += 32) {
         const int cnt = (int)min((int64_t)32, p1 - base);
@@ -145,10 +150,10 @@ __global__ void __launch_bounds__(128) csr_yt_chunk_v4x_kernel(
                 const int c = lane + 32 * q;
                 if (c < nq) {
                     const float4 f = __ldg(f4 + c);
-                    a[q][0] = fma((TY)f.x, (TY)v, a[q][0]);
-                    a[q][1] = fma((TY)f.y, (TY)v, a[q][1]);
-                    a[q][2] = fma((TY)f.z, (TY)v, a[q][2]);
-                    a[q][3] = fma((TY)f.w, (TY)v, a[q][3]);
+                    a[q][0] = fma((TA)f.x, (TA)v, a[q][0]);
+                    a[q][1] = fma((TA)f.y, (TA)v, a[q][1]);
+                    a[q][2] = fma((TA)f.z, (TA)v, a[q][2]);
+                    a[q][3] = fma((TA)f.w, (TA)v, a[q][3]);
                 }
             }
         }
@@ -158,22 +163,27 @@ __global__ void __launch_bounds__(128) csr_yt_chunk_v4x_kernel(
         const int c = lane + 32 * q;
         if (c < nq) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) out[4 * c + t] = a[q][t];
+            for (int t = 0; t < 4; ++t) {
+                if (slot < 0)
+                    outy[4 * c + t] = (TY)a[q][t];
+                else
+                    outp[4 * c + t] = a[q][t];
+            }
         }
     }
 }
 
-template <typename TY>
+template <typename TA, typename TY>
 __global__ void csr_fold_kernel(const int64_t *__restrict__ heavy, int64_t nheavy, int r,
-                                const TY *__restrict__ part, TY *__restrict__ YT) {
+                                const TA *__restrict__ part, TY *__restrict__ YT) {
     const int64_t hv = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (hv >= nheavy) return;
     const int lane = threadIdx.x & 31;
     const int64_t row = heavy[hv * 3 + 0], s0 = heavy[hv * 3 + 1], ns = heavy[hv * 3 + 2];
     for (int i = lane; i < r; i += 32) {
-        TY s = part[s0 * r + i];
+        TA s = part[s0 * r + i];
         for (int64_t k = 1; k < ns; ++k) s += part[(s0 + k) * r + i];
-        YT[row * r + i] = s;
+        YT[row * r + i] = (TY)s;
     }
 }
 
@@ -224,19 +234,19 @@ int csc_linear_vec_launch(const int64_t *indptr, const int64_t *seg, int nblk,
 template <typename TY>
 static int csr_vec_go(const int64_t *chunks, int64_t nchunks, const int64_t *heavy, int64_t nheavy,
                       const int64_t *seg, int nblk, const int32_t *colidx, const float *vals,
-                      const float *FT, int r, TY *YT, TY *part, cudaStream_t st) {
+                      const float *FT, int r, TY *YT, double *part, cudaStream_t st) {
     const dim3 grid((unsigned)((nchunks + 3) / 4));
     for (int b = 0; b < (seg ? nblk : 1); ++b) {
         if (r <= 128)
-            csr_yt_chunk_v4x_kernel<TY, 1><<<grid, 128, 0, st>>>(chunks, nchunks, seg, nblk, b,
-                                                                 colidx, vals, FT, r, YT, part);
+            csr_yt_chunk_v4x_kernel<double, TY, 1><<<grid, 128, 0, st>>>(
+                chunks, nchunks, seg, nblk, b, colidx, vals, FT, r, YT, part);
         else
-            csr_yt_chunk_v4x_kernel<TY, 2><<<grid, 128, 0, st>>>(chunks, nchunks, seg, nblk, b,
-                                                                 colidx, vals, FT, r, YT, part);
+            csr_yt_chunk_v4x_kernel<double, TY, 2><<<grid, 128, 0, st>>>(
+                chunks, nchunks, seg, nblk, b, colidx, vals, FT, r, YT, part);
     }
     if (nheavy > 0)
-        csr_fold_kernel<TY><<<(unsigned)((nheavy + 3) / 4), 128, 0, st>>>(heavy, nheavy, r, part,
-                                                                          YT);
+        csr_fold_kernel<double, TY><<<(unsigned)((nheavy + 3) / 4), 128, 0, st>>>(
+            heavy, nheavy, r, part, YT);
     return launch_status();
 }
 
@@ -246,11 +256,12 @@ int csr_yt_chunked_vec_launch(const int64_t *chunks, int64_t nchunks, const int6
                               void *part, cudaStream_t st) {
     if (nchunks <= 0) return NMFB_OK;
     if (!sparse_vec_ok(r, FT, FT) || nblk < 1) return NMFB_ERR_ARG;
+    // fp64 accumulation (and fp64 heavy-row partials) for either output type
     if (yt_dtype == NMFB_F64)
         return csr_vec_go<double>(chunks, nchunks, heavy, nheavy, seg, nblk, colidx, vals, FT, r,
                                   (double *)YT, (double *)part, st);
     return csr_vec_go<float>(chunks, nchunks, heavy, nheavy, seg, nblk, colidx, vals, FT, r,
-                             (float *)YT, (float *)part, st);
+                             (float *)YT, (double *)part, st);
 }
 
 }  // namespace nmfb

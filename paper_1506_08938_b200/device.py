@@ -413,7 +413,18 @@ class Alternation:
             self.ybuf = torch.empty((self.splits_m * n * r,), dtype=torch.float32, device=dev)
         else:
             self.hbuf = torch.empty((m * r,), dtype=dt, device=dev)
-            ydt = f64 if (data.kind == "sparse" or precision == "fp64") else dt
+            # sparse fast path: Y^T accumulated in fp64 inside the kernel and
+            # stored fp32 (the M-step reads it as fp32 anyway; half the bytes).
+            # fp64 when the X F^T pass is L2-blocked (NMFB_SPMM_BLOCK_MB_F: its
+            # running sums are carried through Y^T between block passes) or on
+            # request (NMFB_YT64=1)
+            import os
+
+            yt64 = (precision == "fp64" or self.mode != L.MODE_FAST
+                    or os.environ.get("NMFB_YT64", "0") == "1"
+                    or (data.kind == "sparse" and self.prec == "fp32" and r % 4 == 0
+                        and r <= 256 and data.spmm_blocking(r)[2] > 1))
+            ydt = f64 if yt64 else dt
             self.ybuf = torch.empty((n * r,), dtype=ydt, device=dev)
         self.max_iters = max_iters
         # per iteration: stats [2 steps][inner, fail], objective pieces
@@ -558,7 +569,8 @@ class Alternation:
             if self.mode == L.MODE_FAST:
                 # load-balanced row chunks (Zipf-popular rows hold 10^4+ entries)
                 if getattr(self, "ypart", None) is None:
-                    self.ypart = torch.empty((max(d.nslots, 1) * r,), dtype=self.ybuf.dtype,
+                    # heavy-row chunk partials: fp64 whatever the Y^T type
+                    self.ypart = torch.empty((max(d.nslots, 1) * r,), dtype=torch.float64,
                                              device=self.ybuf.device)
                 nbf, segf = self._spmm_plan()[2:]
                 if nbf > 1:
@@ -634,7 +646,8 @@ class Alternation:
                    vp(self.FT), self.r, vp(p[0:1]), vp(self.res_ws), self._st())
         else:
             # trace identity (matrix.py:240-253): cross = <G, Y^T>, quad = <G^T G, F F^T>
-            self.dot(self.G, self.code, self.ybuf, L.F64, self.n * self.r, p[1:4])
+            ycode = L.F64 if self.ybuf.dtype == torch.float64 else L.F32
+            self.dot(self.G, self.code, self.ybuf, ycode, self.n * self.r, p[1:4])
             self.gram(self.G, self.n, self.Qg)
             self.qg_valid = True  # reused by the next coefficient step
             self.dot(self.Qg, L.F64, self.Hf, L.F64, self.r * self.r, p[7:10])

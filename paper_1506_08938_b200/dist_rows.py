@@ -244,7 +244,7 @@ class RowCudaEngine:
             return
         ycode = L.F64 if st.ybuf.dtype == torch.float64 else L.F32
         if getattr(st, "ypart", None) is None:
-            st.ypart = torch.empty((max(d.nslots, 1) * r,), dtype=st.ybuf.dtype,
+            st.ypart = torch.empty((max(d.nslots, 1) * r,), dtype=torch.float64,
                                    device=st.ybuf.device)
         L.call("nmfb_csr_yt_chunked", st.code, D.vp(d.chunks), d.nchunks, D.vp(d.heavy),
                d.nheavy, D.vp(d.colidx), D.vp(d.cvals), D.vp(st.FT), r, ycode, D.vp(st.ybuf),

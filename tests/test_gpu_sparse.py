@@ -89,6 +89,9 @@ def test_blocked_spmm_bit_identical(r, monkeypatch):
     x = generators.sparse_zipf(20000, 8000, 2e-3, 9)
     V = SparseMatrix(x.rows, x.cols, x.indptr, x.indices, x.values, validate=False)
     cfg = NmfConfig(rank=r, max_outer=3, seed=2, rel_change_tol=0.0, precision="fp32")
+    # a blocked X F^T carries its running sums through an fp64 Y^T: compare
+    # with the unblocked pass writing fp64 Y^T too
+    monkeypatch.setenv("NMFB_YT64", "1")
     monkeypatch.setenv("NMFB_SPMM_BLOCK_MB", "0")
     monkeypatch.setenv("NMFB_SPMM_BLOCK_MB_F", "0")
     m0, l0 = FitSession(V, cfg).run()
