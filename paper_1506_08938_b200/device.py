@@ -268,9 +268,10 @@ class DeviceData:
         """L2 blocking plan of the sparse data products for rank r (fp32):
         (nblk_g, seg_g, nblk_f, seg_f) -- the gathered factor (G, n x r, for
         G^T X; F^T, m x r, for X F^T) is cut into blocks of at most
-        NMFB_SPMM_BLOCK_MB (G; default 96) / NMFB_SPMM_BLOCK_MB_F (F^T;
+        NMFB_SPMM_BLOCK_MB (G; default 64) / NMFB_SPMM_BLOCK_MB_F (F^T;
         default 0 = off) MB; one block means no blocking.  Measured at config
-        5 (G 800 MB, F^T 160 MB): G^T X 7.0 -> 5.9 ms with 96 MB blocks; the
+        5 (G 800 MB, F^T 160 MB): G^T X 7.0 -> 5.9 ms with 96 MB blocks, 5.86
+        with 64 MB, 6.04 with 128 MB; the
         X F^T pass gets slower blocked (its outputs, n x r = 800 MB, would be
         re-read and re-written every pass), so it stays unblocked."""
         import os
@@ -278,7 +279,7 @@ class DeviceData:
         if r in self.blocking:
             return self.blocking[r]
         plan = []
-        for rows, build, var, dflt in ((self.n, "csc", "NMFB_SPMM_BLOCK_MB", "96"),
+        for rows, build, var, dflt in ((self.n, "csc", "NMFB_SPMM_BLOCK_MB", "64"),
                                        (self.m, "chunk", "NMFB_SPMM_BLOCK_MB_F", "0")):
             mb = float(os.environ.get(var, dflt))
             nblk = max(1, int(np.ceil(rows * r * 4 / (mb * 2**20)))) if mb > 0 else 1
