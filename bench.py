@@ -442,8 +442,16 @@ def run_ours(args):
         fl = 2.0 * R * R * (1 + 2 * kbar) * (m_solve + n_solve)  # this rank's solves
         nn_ms = t / args.steps  # both NNLS launches of one step
         ach = fl / (nn_ms / 1e3) / 1e12
+        # E-only / M-only rates: the step's two NNLS launches in order
+        src_rec = cnt if sparse else rec
+        seq = [a.elapsed_time(b) for nm, a, b in src_rec.calls if nm in nn_names]
+        e_ms = sum(seq[0::2]) / max(len(seq[0::2]), 1)
+        m_ms = sum(seq[1::2]) / max(len(seq[1::2]), 1)
         rooflines["nnls"] = {
             "kernel": "nmfb_nnls_batch (E + M solves of one step)", "bound": "fp32",
+            "e_step_ms": e_ms, "m_step_ms": m_ms,
+            "e_solves_per_s": m_solve / (e_ms / 1e3) if e_ms else None,
+            "m_solves_per_s": n_solve / (m_ms / 1e3) if m_ms else None,
             "achieved": ach, "peak": ffma_tf, "unit": "TFLOP/s", "frac": ach / ffma_tf,
             "peak_source": micro_src, "algorithmic_flops_per_step": fl, "k_bar": kbar,
             "ms_per_step": nn_ms, "avg_launch_ms": nn_ms / 2, "share":

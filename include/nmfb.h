@@ -364,6 +364,29 @@ int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *in
                       const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
                       void *stream);
 
+/* Collectives of the multi-GPU layouts (NCCL over
+ * NVLink, resolved at run time from libnccl.so.2 -- the NCCL a PyTorch process
+ * already holds).  The reference has no transport ("one would slot in",
+ * parallel.py:9-12); these are the exchanges of paper_1506_08938_b200/
+ * dist_rows.py's row-sharded layout.
+ *   nmfb_comm_available      1 if NCCL could be resolved
+ *   nmfb_comm_unique_id      128-byte id (rank 0 creates, every rank passes it)
+ *   nmfb_comm_init           one communicator per rank (collective)
+ *   nmfb_allreduce_r2        in-place fp64 sum (r x r Grams, objective pieces)
+ *   nmfb_reduce_scatter_panel   sum of world panels of world*recv_count
+ *                               elements, block g -> rank g (fp32 / fp64)
+ *   nmfb_allgather_panel     send_count elements per rank -> every rank
+ * Stream-ordered on `stream`. */
+int nmfb_comm_available(void);
+int nmfb_comm_unique_id(void *id_out);
+int nmfb_comm_init(const void *id, int32_t rank, int32_t nranks, void **comm_out);
+int nmfb_comm_destroy(void *comm);
+int nmfb_allreduce_r2(void *comm, double *buf, int64_t count, void *stream);
+int nmfb_reduce_scatter_panel(void *comm, const void *send, void *recv, int64_t recv_count,
+                              int dtype, void *stream);
+int nmfb_allgather_panel(void *comm, const void *send, void *recv, int64_t send_count, int dtype,
+                         void *stream);
+
 /* Return the ingest kernels' cached scratch (a private stream-ordered pool on
  * the current device, kept mapped between ingests) to the driver.  Waits for
  * the device. */

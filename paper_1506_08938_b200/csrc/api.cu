@@ -39,6 +39,15 @@ int csc_validate_launch(int64_t rows, int64_t cols, int64_t nnz, const int64_t *
                         const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
                         cudaStream_t st);
 int ingest_release_scratch();
+int comm_available();
+int comm_unique_id(void *id);
+int comm_init(const void *id, int rank, int nranks, void **comm);
+int comm_destroy(void *comm);
+int allreduce_r2(void *comm, double *buf, int64_t count, cudaStream_t st);
+int reduce_scatter_panel(void *comm, const void *send, void *recv, int64_t recv_count, int dtype,
+                         cudaStream_t st);
+int allgather_panel(void *comm, const void *send, void *recv, int64_t send_count, int dtype,
+                    cudaStream_t st);
 int nqp_step_launch(int op, const double *Q, int r, const double *x, const double *g,
                     int64_t count, int sweeps, double *xo, double *go, cudaStream_t st);
 int narrow_indices_launch(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
@@ -489,6 +498,24 @@ int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *in
 }
 
 int nmfb_ingest_release_scratch(void) { return check(ingest_release_scratch()); }
+
+int nmfb_comm_available(void) { return comm_available(); }
+int nmfb_comm_unique_id(void *id_out) { return check(comm_unique_id(id_out)); }
+int nmfb_comm_init(const void *id, int32_t rank, int32_t nranks, void **comm_out) {
+    return check(comm_init(id, rank, nranks, comm_out));
+}
+int nmfb_comm_destroy(void *comm) { return check(comm_destroy(comm)); }
+int nmfb_allreduce_r2(void *comm, double *buf, int64_t count, void *stream) {
+    return check(allreduce_r2(comm, buf, count, (cudaStream_t)stream));
+}
+int nmfb_reduce_scatter_panel(void *comm, const void *send, void *recv, int64_t recv_count,
+                              int dtype, void *stream) {
+    return check(reduce_scatter_panel(comm, send, recv, recv_count, dtype, (cudaStream_t)stream));
+}
+int nmfb_allgather_panel(void *comm, const void *send, void *recv, int64_t send_count, int dtype,
+                         void *stream) {
+    return check(allgather_panel(comm, send, recv, send_count, dtype, (cudaStream_t)stream));
+}
 
 int nmfb_narrow_indices(const int64_t *in, int64_t n, int32_t *out, int64_t *info,
                         void *stream) {

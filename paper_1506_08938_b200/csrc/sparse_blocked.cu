@@ -47,7 +47,7 @@ __global__ void segments_kernel(int64_t nout, const int64_t *__restrict__ lo_of,
 }
 
 #ifndef NMFB_CSC_MINB
-#define NMFB_CSC_MINB 1
+#define NMFB_CSC_MINB 12  // <= 40 registers: C5 G^T X 5.85 -> 5.67 ms (16: spills, 8.1)
 #endif
 template <int NV>
 __global__ void __launch_bounds__(128, NMFB_CSC_MINB) csc_linear_v4x_kernel(
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(128, NMFB_CSC_MINB) csc_linear_v4x_kernel(
 // TA: accumulation type (the heavy-row chunk partials too), TY: the Y^T
 // output (fp32 Y^T is accumulated in fp64 and rounded once)
 #ifndef NMFB_CSR_MINB
-#define NMFB_CSR_MINB 8  // <= 64 registers: C5 X F^T 9.07 -> 7.23 ms (occupancy)
+#define NMFB_CSR_MINB 10  // <= 48 registers: C5 X F^T 9.07 -> 6.70 ms (occupancy; 8: 7.24)
 #endif
 template <typename TA, typename TY, int NV>
 __global__ void __launch_bounds__(128, NMFB_CSR_MINB) csr_yt_chunk_v4x_kernel(

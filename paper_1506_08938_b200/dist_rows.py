@@ -90,25 +90,79 @@ def csc_row_block(X, lo, hi):
     return hi - lo, X.cols, indptr, idx[keep] - lo, np.asarray(X.values)[keep]
 
 
-class RowShardedAlternation:
-    """One rank's share of the alternation in the row layout."""
+class NativeComm:
+    """The C-ABI collectives (nmfb_comm_init / allreduce_r2 /
+    reduce_scatter_panel / allgather_panel, csrc/comm.cu): one NCCL
+    communicator per rank, its unique id handed out through the
+    torch.distributed group; stream-ordered on the current stream."""
 
-    def __init__(self, engine, plan: RowPlan, rank, group=None):
+    def __init__(self, group=None):
+        import ctypes
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if not L.lib().nmfb_comm_available():
+            raise RuntimeError("libnccl.so.2 could not be resolved")
+        uid = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            L.call("nmfb_comm_unique_id", uid.ctypes.data_as(ctypes.c_void_p))
+        t = torch.from_numpy(uid)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, 0, group=group)
+        uid = t.cpu().numpy()
+        self.handle = ctypes.c_void_p()
+        L.call("nmfb_comm_init", uid.ctypes.data_as(ctypes.c_void_p), self.rank, self.world,
+               ctypes.byref(self.handle))
+
+    def allreduce(self, t):
+        assert t.dtype == torch.float64 and t.is_contiguous()
+        L.call("nmfb_allreduce_r2", self.handle, D.vp(t), t.numel(), D.stream_handle())
+        return t
+
+    def reduce_scatter(self, full, out):
+        code = L.F32 if out.dtype == torch.float32 else L.F64
+        L.call("nmfb_reduce_scatter_panel", self.handle, D.vp(full), D.vp(out), out.numel(),
+               code, D.stream_handle())
+        return out
+
+    def allgather(self, full, mine):
+        code = L.F32 if full.dtype == torch.float32 else L.F64
+        L.call("nmfb_allgather_panel", self.handle, D.vp(mine), D.vp(full), mine.numel(), code,
+               D.stream_handle())
+        return full
+
+    def close(self):
+        if getattr(self, "handle", None):
+            L.call("nmfb_comm_destroy", self.handle)
+            self.handle = None
+
+
+class RowShardedAlternation:
+    """One rank's share of the alternation in the row layout.  Collectives:
+    the C-ABI NCCL ones (NativeComm) when given, else torch.distributed."""
+
+    def __init__(self, engine, plan: RowPlan, rank, group=None, native=None):
         self.e = engine
         self.plan = plan
         self.rank = rank
         self.group = group
+        self.native = native
         self.comm = dist.is_available() and dist.is_initialized()
         if not self.comm and plan.world != 1:
             raise RuntimeError("world > 1 needs an initialised torch.distributed group")
         self.qg_valid = False
 
     def _allreduce(self, t):
+        if self.native is not None:
+            return self.native.allreduce(t)
         if self.comm:
             dist.all_reduce(t, group=self.group)
         return t
 
     def _reduce_scatter(self, full, out):
+        if self.native is not None:
+            return self.native.reduce_scatter(full, out)
         if self.comm:
             dist.reduce_scatter_tensor(out, full, group=self.group)
         else:
@@ -116,9 +170,12 @@ class RowShardedAlternation:
         return out
 
     def _allgather(self, full):
+        c = self.plan.col_chunk
+        mine = full[self.rank * c: (self.rank + 1) * c]
+        if self.native is not None:
+            # in place: my block already sits at full + rank * chunk
+            return self.native.allgather(full, mine)
         if self.comm:
-            c = self.plan.col_chunk
-            mine = full[self.rank * c: (self.rank + 1) * c]
             dist.all_gather_into_tensor(full, mine, group=self.group)
         return full
 
@@ -296,8 +353,16 @@ class RowShardedFit:
         G0, FT0 = init
         self.engine = RowCudaEngine(Xr, cfg, np.asarray(G0)[lo:hi], FT0, self.plan, rank,
                                     cfg.max_outer)
-        self.state = _RowStateView(RowShardedAlternation(self.engine, self.plan, rank, group),
-                                   self.engine.st)
+        # collectives: the C-ABI NCCL ones by default on an NCCL group
+        # (NMFB_COMM=torch: torch.distributed's)
+        import os
+
+        self.native = None
+        if (dist.is_initialized() and dist.get_backend(group) == "nccl"
+                and os.environ.get("NMFB_COMM", "native") == "native"):
+            self.native = NativeComm(group)
+        self.state = _RowStateView(RowShardedAlternation(self.engine, self.plan, rank, group,
+                                                         native=self.native), self.engine.st)
         self.peer = False
 
 

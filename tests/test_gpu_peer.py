@@ -247,9 +247,50 @@ def test_dist_world1_sparse_block_equals_single_gpu(tmp_path):
     assert res["G_equal"] and res["FT_equal"] and res["obj_equal"], res
 
 
-def test_dist_world1_row_sharded_sparse_equals_single_gpu(tmp_path):
+@pytest.mark.parametrize("comm", ["native", "torch"])
+def test_dist_world1_row_sharded_sparse_equals_single_gpu(tmp_path, comm):
     """torchrun, one rank, the ROW-sharded layout for tall sparse data
     (dist_rows.py: Gram / H_f allreduces, reduce-scatter of the partial linear
-    terms, allgather of F over NCCL): bit-identical to the single-GPU fit."""
-    res = _torchrun({"NMFB_CHECK_ROWS": "1"}, tmp_path, "rows")
+    terms, allgather of F over NCCL -- through the C-ABI collectives
+    nmfb_comm_init / allreduce_r2 / reduce_scatter_panel / allgather_panel, or
+    torch.distributed's): bit-identical to the single-GPU fit."""
+    res = _torchrun({"NMFB_CHECK_ROWS": "1", "NMFB_COMM": comm}, tmp_path, "rows_" + comm)
     assert res["G_equal"] and res["FT_equal"] and res["obj_equal"], res
+
+
+def test_comm_c_abi_single_rank():
+    """The C-ABI collectives (csrc/comm.cu) on a one-rank NCCL communicator:
+    allreduce / reduce-scatter / allgather are the identity (in-place
+    allgather included); argument errors are rejected."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    assert L.lib().nmfb_comm_available() == 1
+    uid = np.zeros(128, dtype=np.uint8)
+    L.call("nmfb_comm_unique_id", uid.ctypes.data_as(ctypes.c_void_p))
+    comm = ctypes.c_void_p()
+    L.call("nmfb_comm_init", uid.ctypes.data_as(ctypes.c_void_p), 0, 1, ctypes.byref(comm))
+    try:
+        a = torch.arange(40, dtype=torch.float64, device=dev)
+        want = a.clone()
+        L.call("nmfb_allreduce_r2", comm, D.vp(a), a.numel(), D.stream_handle())
+        full = torch.randn(64, 8, device=dev)
+        out = torch.empty(64, 8, device=dev)
+        L.call("nmfb_reduce_scatter_panel", comm, D.vp(full), D.vp(out), out.numel(), L.F32,
+               D.stream_handle())
+        g = full.clone()
+        L.call("nmfb_allgather_panel", comm, D.vp(g), D.vp(g), g.numel(), L.F32,
+               D.stream_handle())
+        torch.cuda.synchronize()
+        assert torch.equal(a, want) and torch.equal(out, full) and torch.equal(g, full)
+        with pytest.raises(ValueError):
+            L.call("nmfb_reduce_scatter_panel", comm, D.vp(full), D.vp(out), 8, 7,
+                   D.stream_handle())
+    finally:
+        L.call("nmfb_comm_destroy", comm)
