@@ -11,6 +11,10 @@
 #define NMFB_NNLS_EXACT_ARGMAX 1
 #endif
 
+#ifndef NMFB_NNLS_DCARRY
+#define NMFB_NNLS_DCARRY 0  // measured slower: r=200 1.67 -> 1.82 ms
+#endif
+
 #ifndef NMFB_NNLS_YSMEM
 #define NMFB_NNLS_YSMEM 0
 #endif
@@ -242,6 +246,8 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
     // r = 200 1.84 -> 2.02 ms -- the per-selection y reload lengthens the
     // dependency chain more than the removed owner select saves)
     constexpr bool YSMEM = NMFB_NNLS_EXACT_ARGMAX && NMFB_NNLS_YSMEM;
+    // the winner's step carried through the exact argmax tree (see the CD)
+    constexpr bool DCARRY = NMFB_NNLS_EXACT_ARGMAX && (YSMEM || NMFB_NNLS_DCARRY);
     extern __shared__ __align__(16) float smem_f[];
     float *Qs = smem_f;                          // R x SP, permuted rows (see nnls_ep)
     __shared__ float blk_norm[B][32], blk_final[B][32];
@@ -617,7 +623,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                     auto ycur = [&](int e) { if constexpr (YSMEM) return yv[e]; else return y[e]; };
                     unsigned key[EE];
                     int ix[EE];
-                    float dv[YSMEM ? EE : 1];
+                    float dv[DCARRY ? EE : 1];
 #pragma unroll
                     for (int e = 0; e < EE; e += 2) {
                         const float d0 = -fminf(gr[e], ycur(e)), d1 = -fminf(gr[e + 1], ycur(e + 1));
@@ -628,7 +634,7 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                         key[e + 1] = __float_as_uint(dc.y);
                         ix[e] = e;
                         ix[e + 1] = e + 1;
-                        if constexpr (YSMEM) {
+                        if constexpr (DCARRY) {
                             dv[e] = d0;
                             dv[e + 1] = d1;
                         }
@@ -640,9 +646,9 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                             const bool keep = key[e] >= key[e + w];
                             key[e] = keep ? key[e] : key[e + w];
                             ix[e] = keep ? ix[e] : ix[e + w];
-                            if constexpr (YSMEM) dv[e] = keep ? dv[e] : dv[e + w];
+                            if constexpr (DCARRY) dv[e] = keep ? dv[e] : dv[e + w];
                         }
-                    if constexpr (YSMEM) dwin = dv[0];
+                    if constexpr (DCARRY) dwin = dv[0];
                     unsigned long long kb = ((unsigned long long)key[0] << 32) |
                                             ((unsigned)(EE - 1 - ix[0]) << LB) | lcode;
 #pragma unroll
@@ -700,6 +706,16 @@ __global__ void __launch_bounds__(32 * L * B, nnls_min_blocks(E, L, 32 * L * B))
                         // d = -min(g, y) of the winning coordinate
                         pdx = (L == 1) ? dwin : __shfl_sync(gmask, dwin, lp, L);
                         if (l == lp) ys[ep] += pdx;
+                    } else if constexpr (DCARRY) {
+                        // the winner's step d = -min(g, y) comes with the argmax
+                        // (carried through the tree), so the owner's update is
+                        // independent per register -- no dependent select chain
+                        // on the way to the next selection's row axpy
+                        pdx = (L == 1) ? dwin : __shfl_sync(gmask, dwin, lp, L);
+                        const int epo = (l == lp) ? ep : -1;
+#pragma unroll
+                        for (int e = 0; e < E; ++e)
+                            if (e == epo) y[e] += pdx;
                     } else {
                         float dxo = 0.f;
 #pragma unroll

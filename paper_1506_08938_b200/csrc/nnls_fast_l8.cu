@@ -4,7 +4,7 @@
 
 namespace nmfb {
 
-#define NMFB_VARIANTS_L8(X) X(7, 8, 1) X(13, 8, 1) X(16, 8, 1) X(25, 8, 1) X(28, 8, 1)
+#define NMFB_VARIANTS_L8(X) X(7, 8, 1) X(8, 8, 1) X(13, 8, 1) X(16, 8, 1) X(25, 8, 1) X(28, 8, 1)
 
 // smallest E with E * 8 >= need; returns E or 0
 int fast_pick_l8(int need) {
