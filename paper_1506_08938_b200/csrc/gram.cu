@@ -140,9 +140,13 @@ static int64_t gram_chunk(int64_t rows) {
     return chunk;
 }
 
+// Workspace for any call with at most `rows` rows: the chunk count is at most
+// min(ceil(rows / GROWS), 296) -- monotone in rows (the actual count is not:
+// fewer rows can mean more, smaller chunks), so one workspace sized for the
+// largest operand serves the Grams of both factors.
 size_t gram_workspace_bytes(int64_t rows, int r) {
-    int64_t chunk = gram_chunk(rows);
-    int64_t nchunk = rows > 0 ? (rows + chunk - 1) / chunk : 1;
+    int64_t nchunk = rows > 0 ? (rows + GROWS - 1) / GROWS : 1;
+    if (nchunk > 296) nchunk = 296;
     return (size_t)nchunk * r * r * sizeof(double) + 64;  // + the fused-rescale ticket
 }
 

@@ -44,6 +44,14 @@ def tc_enabled():
     return os.environ.get("NMFB_DISABLE_TC", "0") != "1"
 
 
+def gram_overlap_enabled():
+    """Sparse path: Grams on a side stream beside the sparse data products,
+    unless NMFB_GRAM_OVERLAP=0."""
+    import os
+
+    return os.environ.get("NMFB_GRAM_OVERLAP", "1") != "0"
+
+
 def d_i8_enabled():
     """Exact int8 tensor-core residual unless NMFB_DISABLE_I8=1 (A/B comparisons)."""
     import os
@@ -328,7 +336,7 @@ class Alternation:
     """Device state of fit(): G (n, r), FT (m, r) and all step buffers."""
 
     def __init__(self, data: DeviceData, cfg, G0, FT0, max_iters, precision="fp32", lanes=0,
-                 kernel_mode=None, splits=None, solver="nnls"):
+                 kernel_mode=None, splits=None, solver="nnls", overlap=True):
         self.d = data
         self.cfg = cfg
         # solver "mur": the multiplicative-update baseline (baselines.py:41-85)
@@ -370,6 +378,16 @@ class Alternation:
         self.ra = [torch.zeros((1,), dtype=torch.int32, device=dev) for _ in range(2)]
         self.gram_ws = torch.empty((L.lib().nmfb_gram_workspace_bytes(max(n, m), r) // 8 + 1,),
                                    dtype=f64, device=dev)
+        # sparse fp32 path: the Grams (FMA-bound) run on a side stream beside
+        # the L2-bound sparse data products that do not need them (see estep)
+        self.gside = None
+        if (data.kind == "sparse" and self.mode == L.MODE_FAST and overlap
+                and gram_overlap_enabled()):
+            self.gside = torch.cuda.Stream(device=dev)
+            self.gside_ev = None      # Q_g (Gram of G) + objective quad ready
+            self.hf_ev = None         # H_f (Gram of F) + its rescale ready
+            self.dot_ws2 = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,),
+                                       dtype=f64, device=dev)
         self.dot_ws = torch.empty((L.lib().nmfb_dot_workspace_bytes(0) // 8 + 1,), dtype=f64,
                                   device=dev)
         sms = max(L.lib().nmfb_device_sm_count(), 1)
@@ -489,9 +507,25 @@ class Alternation:
                float(self.cfg.epsilon), int(self.cfg.inner_cap), 0.0, None, None, vp(stats),
                self.lanes, self._st())
 
-    def dot(self, a, a_code, b, b_code, length, out):
-        L.call("nmfb_dot", vp(a), a_code, vp(b), b_code, length, vp(out), vp(self.dot_ws),
-               self._st())
+    def dot(self, a, a_code, b, b_code, length, out, ws=None):
+        L.call("nmfb_dot", vp(a), a_code, vp(b), b_code, length, vp(out),
+               vp(self.dot_ws if ws is None else ws), self._st())
+
+    def _overlap(self):
+        """The side stream for the Grams, or None (off, or serialised timing)."""
+        return None if (self.gside is None or getattr(self, "serial", False)) else self.gside
+
+    def _on_side(self):
+        """Side stream ordered after the work enqueued so far on the caller's."""
+        ev = torch.cuda.Event()
+        ev.record()
+        self.gside.wait_event(ev)
+        return torch.cuda.stream(self.gside)
+
+    def _side_done(self):
+        ev = torch.cuda.Event()
+        ev.record(self.gside)
+        return ev
 
     # -- the two half-steps ---------------------------------------------------
     def estep(self, k):
@@ -499,12 +533,15 @@ class Alternation:
         m columns, then the accumulators H_f = F F^T and Y^T = X F^T."""
         cfg, d, r = self.step_cfg, self.d, self.r
         n, m = self.n, self.m
-        if not self.qg_valid:
-            # Gram of G with the anti-lopsided rescale fused into its epilogue
-            self.gram_rescale(self.G, n, self.Qg, 2.0 * cfg.mu2, 0)
-        else:
-            self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
-        self.qg_valid = False
+        pending_q = d.kind == "sparse" and self.qg_valid and \
+            getattr(self, "gside_ev", None) is not None
+        if not pending_q:
+            if not self.qg_valid:
+                # Gram of G with the anti-lopsided rescale fused into its epilogue
+                self.gram_rescale(self.G, n, self.Qg, 2.0 * cfg.mu2, 0)
+            else:
+                self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
+            self.qg_valid = False
         st = self.stats[k, 0]
         if d.kind == "dense":
             if self.use_tc:
@@ -535,12 +572,24 @@ class Alternation:
             else:
                 L.call("nmfb_csc_linear", self.code, self.mode, vp(d.indptr), vp(d.rowidx),
                        vp(d.vals), 0, m, vp(self.G), r, cfg.mu1, vp(self.hbuf), self._st())
+            if pending_q:
+                # Q_g came from the side stream (overlapping the data product above)
+                torch.cuda.current_stream().wait_event(self.gside_ev)
+                self.gside_ev = None
+                self.rescale(self.Qg, 2.0 * cfg.mu2, 0)
+                self.qg_valid = False
             self.nnls(0, self.hbuf, self.code, 0, r, 0, 0.0, self.FT, m, st)
         # accumulators from the new coefficients
         ba, bp = L.bounds_array(self.bounds_e)
         W = len(self.bounds_e) - 1
         if self.prec == "fp64" or self.mode == L.MODE_REFERENCE:
             L.call("nmfb_hp_ref", self.code, vp(self.FT), m, r, bp, W, vp(self.Hf), self._st())
+        elif self._overlap() is not None:
+            # H_f = F F^T (+ rescale) on the side stream, beside X F^T below
+            with self._on_side():
+                self.gram_rescale(self.FT, m, self.Hf, 2.0 * cfg.beta2, 1)
+            self.hf_ev = self._side_done()
+            self.hf_rescaled = True
         else:
             # H_f = F F^T, rescaled for the component step right away
             self.gram_rescale(self.FT, m, self.Hf, 2.0 * cfg.beta2, 1)
@@ -592,6 +641,9 @@ class Alternation:
         """Component step (parallel.run_mstep): NNLS over the n rows with
         h = beta1 - Y^T."""
         cfg = self.step_cfg
+        if getattr(self, "hf_ev", None) is not None:
+            torch.cuda.current_stream().wait_event(self.hf_ev)
+            self.hf_ev = None
         if not getattr(self, "hf_rescaled", False):
             self.rescale(self.Hf, 2.0 * cfg.beta2, 1)
         self.hf_rescaled = False
@@ -649,9 +701,18 @@ class Alternation:
             # trace identity (matrix.py:240-253): cross = <G, Y^T>, quad = <G^T G, F F^T>
             ycode = L.F64 if self.ybuf.dtype == torch.float64 else L.F32
             self.dot(self.G, self.code, self.ybuf, ycode, self.n * self.r, p[1:4])
-            self.gram(self.G, self.n, self.Qg)
+            if self._overlap() is not None:
+                # G^T G and the quad term on the side stream: they overlap the
+                # next coefficient step's G^T X, which does not need them
+                with self._on_side():
+                    self.gram(self.G, self.n, self.Qg)
+                    self.dot(self.Qg, L.F64, self.Hf, L.F64, self.r * self.r, p[7:10],
+                             ws=self.dot_ws2)
+                self.gside_ev = self._side_done()
+            else:
+                self.gram(self.G, self.n, self.Qg)
+                self.dot(self.Qg, L.F64, self.Hf, L.F64, self.r * self.r, p[7:10])
             self.qg_valid = True  # reused by the next coefficient step
-            self.dot(self.Qg, L.F64, self.Hf, L.F64, self.r * self.r, p[7:10])
         # penalty sums: slots 4..6 = (-, sum|F|, sum F^2); 1..3 = (cross, sum|G|, sum G^2)
         if cfg.mu1 or cfg.mu2:
             self.dot(self.FT, self.code, None, L.F64, self.m * self.r, p[4:7])
@@ -674,6 +735,8 @@ class Alternation:
                 for q in (0, 1):
                     self._wait_residual(q)
             torch.cuda.current_stream().wait_stream(main)
+        if getattr(self, "gside", None) is not None:
+            torch.cuda.current_stream().wait_stream(self.gside)
 
     def snapshot(self):
         """Copy G, F^T (the state after the last enqueued iteration) into
@@ -702,6 +765,19 @@ class Alternation:
         (both steps and its objective pieces) is done, without making the
         step streams wait."""
         cur = torch.cuda.current_stream()
+        if getattr(self, "gside", None) is not None:
+            # sparse overlap: observe the step stream and the side-stream Grams
+            # from an auxiliary stream, so the next iteration's G^T X is not
+            # held back behind the Gram it overlaps
+            if getattr(self, "obs", None) is None:
+                self.obs = torch.cuda.Stream(device=self.G.device)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self.obs.wait_event(ev)
+            self.obs.wait_stream(self.gside)
+            done = torch.cuda.Event(enable_timing=True)
+            done.record(self.obs)
+            return done
         main = getattr(self, "main", None)
         if main is not None:
             ev = torch.cuda.Event()

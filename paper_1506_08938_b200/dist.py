@@ -237,7 +237,7 @@ class CudaEngine:
     def __init__(self, X_block, cfg, G0, FT0_block, max_iters, n_total_cols):
         self.data = D.DeviceData(X_block, cfg.precision)
         self.st = D.Alternation(self.data, cfg, G0, FT0_block, max_iters,
-                                precision=cfg.precision, lanes=cfg.lanes)
+                                precision=cfg.precision, lanes=cfg.lanes, overlap=False)
         self.cfg = cfg
         self.r = cfg.rank
         st = self.st

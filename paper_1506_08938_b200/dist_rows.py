@@ -221,7 +221,7 @@ class RowCudaEngine:
         # the Alternation supplies the buffers and primitive launches (its G is
         # my row block, its F^T the replicated one)
         self.st = D.Alternation(self.data, cfg, G0_rows, FT0, max_iters, precision="fp32",
-                                lanes=cfg.lanes)
+                                lanes=cfg.lanes, overlap=False)
         self.st.FT = self.ft_pad[:m]
         self.hpad = torch.zeros((plan.padded_cols, r), dtype=torch.float32, device=dev)
         self.hcol = torch.zeros((plan.col_chunk, r), dtype=torch.float32, device=dev)

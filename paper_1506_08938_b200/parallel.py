@@ -75,7 +75,7 @@ def run_estep(V, G, Q_g, cfg, F):
     data = _vt_as_data(V, cfg.precision)
     G = np.asarray(G)
     Qg = Q_g.array if isinstance(Q_g, DenseMatrix) else np.asarray(Q_g)
-    st = D.Alternation(data, cfg, G, F, 1, precision=cfg.precision, lanes=cfg.lanes,
+    st = D.Alternation(data, cfg, G, F, 1, precision=cfg.precision, lanes=cfg.lanes, overlap=False,
                        splits=1)
     st.Qg.copy_(torch.from_numpy(np.ascontiguousarray(Qg, dtype=np.float64)))
     st.qg_valid = True

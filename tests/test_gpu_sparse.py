@@ -103,3 +103,27 @@ def test_blocked_spmm_bit_identical(r, monkeypatch):
     assert np.array_equal(m0.G.array, m1.G.array)
     assert np.array_equal(m0.F.array, m1.F.array)
     assert l0.objective == l1.objective
+
+
+def test_gram_side_stream_overlap_bit_identical(monkeypatch):
+    """The sparse path's Grams on a side stream (beside G^T X / X F^T) give the
+    same bits as the serial order, and the lagged log sees the side-stream
+    objective pieces."""
+    from oracle import generators
+    from paper_1506_08938_b200 import NmfConfig, SparseMatrix
+    from paper_1506_08938_b200.nmf import FitSession
+
+    x = generators.sparse_zipf(20000, 8000, 2e-3, 4)
+    V = SparseMatrix(x.rows, x.cols, x.indptr, x.indices, x.values, validate=False)
+    cfg = NmfConfig(rank=64, max_outer=5, seed=3, rel_change_tol=1e-12, precision="fp32")
+    monkeypatch.setenv("NMFB_GRAM_OVERLAP", "0")
+    s0 = FitSession(V, cfg)
+    assert s0.state.gside is None
+    m0, l0 = s0.run()
+    monkeypatch.setenv("NMFB_GRAM_OVERLAP", "1")
+    s1 = FitSession(V, cfg)
+    assert s1.state.gside is not None
+    m1, l1 = s1.run()
+    assert np.array_equal(m0.G.array, m1.G.array)
+    assert np.array_equal(m0.F.array, m1.F.array)
+    assert l0.objective == l1.objective
