@@ -150,13 +150,17 @@ class DeviceCsc:
             raise MatrixSizeError("sizes must fit the device index types")
         indptr = torch.from_numpy(np.ascontiguousarray(V.indptr, dtype=np.int64)).to(
             device, non_blocking=True)
-        idx64 = torch.from_numpy(np.ascontiguousarray(V.indices, dtype=np.int64)).to(device)
+        from .device import upload_host
+
+        # the big arrays through pinned staging (threaded host copies, the
+        # float64 -> dtype cast on the device)
+        idx64 = upload_host(np.ascontiguousarray(V.indices, dtype=np.int64), torch.int64,
+                            device)
         rowidx = torch.empty(max(V.nnz, 1), dtype=torch.int32, device=device)[: V.nnz]
         info = torch.empty(L.INGEST_CODES, dtype=torch.int64, device=device)
         L.call("nmfb_narrow_indices", _vp(idx64), V.nnz, _vp(rowidx), _vp(info), _stream())
+        vals = upload_host(np.ascontiguousarray(V.values, dtype=np.float64), dtype, device)
         del idx64
-        vals = torch.from_numpy(np.ascontiguousarray(V.values, dtype=np.float64)).to(device)
-        vals = vals.to(dtype)
         if validate:
             raise_for(info.cpu().numpy(), (L.INGEST_ROW_RANGE,))
         return cls(V.rows, V.cols, indptr, rowidx, vals, validate=validate)

@@ -239,14 +239,29 @@ class FitSession:
                 init = device_initial_factors(n, m, D.device_sums(V.values)[0] / (n * m), cfg,
                                               data.device)
         elif data is None:
+            from concurrent.futures import ThreadPoolExecutor
+
             V = _as_matrix(V)
-            require_nonnegative(V, "data matrix")
-            data = D.DeviceData(V, cfg.precision)
+            # the host checks (matrix.py:169-178) and the host mean (numpy's
+            # summation, as nmf.py:109-112 -- the init must be the reference's
+            # bit for bit) run on worker threads while this thread uploads X;
+            # the reference's error still wins over any device-side one
+            with ThreadPoolExecutor(2) as pool:
+                fchk = pool.submit(require_nonnegative, V, "data matrix")
+                fmean = pool.submit(_mean, V) if init is None else None
+                dev_err = None
+                try:
+                    data = D.DeviceData(V, cfg.precision)
+                except Exception as exc:  # noqa: BLE001 -- re-raised below
+                    dev_err = exc
+                fchk.result()
+                if dev_err is not None:
+                    raise dev_err
+                mean = fmean.result() if fmean is not None else None
             n, m = _shape(V)
             if init is None:
-                # the host mean (numpy's summation, as nmf.py:109-112), the
-                # draws on the device
-                init = device_initial_factors(n, m, _mean(V), cfg, data.device)
+                # the draws on the device
+                init = device_initial_factors(n, m, mean, cfg, data.device)
         else:
             n, m = data.n, data.m
             if init is None:
