@@ -46,6 +46,31 @@ __global__ void segments_kernel(int64_t nout, const int64_t *__restrict__ lo_of,
     s[nblk] = p1;
 }
 
+// Streaming hints: the sparse indices / values and the h / Y^T rows are
+// touched once per pass -- load / store them evict-first so they do not push
+// the reused factor rows (G block, F^T) out of L2.
+#ifndef NMFB_SPMM_STREAM_HINTS
+#define NMFB_SPMM_STREAM_HINTS 1
+#endif
+// The outputs only when they exceed L2 (config 5's h / Y^T: 160 / 800 MB);
+// an L2-sized output (config 3) is better left for the NNLS that reads it next.
+#if NMFB_SPMM_STREAM_HINTS
+#define NMFB_LDS_(p) __ldcs(p)
+#define NMFB_STO_(p, v)       \
+    do {                      \
+        if (stream_out)       \
+            __stcs((p), (v)); \
+        else                  \
+            *(p) = (v);       \
+    } while (0)
+#define NMFB_LDO_(p) (stream_out ? __ldcs(p) : *(p))
+#else
+#define NMFB_LDS_(p) (*(p))
+#define NMFB_STO_(p, v) (*(p) = (v))
+#define NMFB_LDO_(p) (*(p))
+#endif
+constexpr int64_t kStreamOutBytes = 64ll << 20;
+
 #ifndef NMFB_CSC_MINB
 #define NMFB_CSC_MINB 12  // <= 40 registers: C5 G^T X 5.85 -> 5.67 ms (16: spills, 8.1)
 #endif
@@ -53,7 +78,8 @@ template <int NV>
 __global__ void __launch_bounds__(128, NMFB_CSC_MINB) csc_linear_v4x_kernel(
     const int64_t *__restrict__ indptr, const int64_t *__restrict__ seg, int nblk, int b,
     const int32_t *__restrict__ rowidx, const float *__restrict__ vals, int64_t col_lo,
-    int64_t col_hi, const float *__restrict__ G, int r, float mu1, float *__restrict__ h) {
+    int64_t col_hi, const float *__restrict__ G, int r, float mu1, float *__restrict__ h,
+    bool stream_out) {
     const int64_t col = col_lo + (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (col >= col_hi) return;
     const int lane = threadIdx.x & 31;
@@ -63,7 +89,7 @@ __global__ void __launch_bounds__(128, NMFB_CSC_MINB) csc_linear_v4x_kernel(
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
         const int c = lane + 32 * q;
-        acc[q] = (b > 0 && c < nq) ? out[c] : make_float4(mu1, mu1, mu1, mu1);
+        acc[q] = (b > 0 && c < nq) ? NMFB_LDO_(out + c) : make_float4(mu1, mu1, mu1, mu1);
     }
     int64_t p0, p1;
     if (seg) {
@@ -78,8 +104,8 @@ __global__ void __launch_bounds__(128, NMFB_CSC_MINB) csc_linear_v4x_kernel(
         int myrow = 0;
         float myv = 0.f;
         if (lane < cnt) {
-            myrow = rowidx[base + lane];
-            myv = vals[base + lane];
+            myrow = NMFB_LDS_(rowidx + base + lane);
+            myv = NMFB_LDS_(vals + base + lane);
         }
 #pragma unroll 8
         for (int u = 0; u < cnt; ++u) {
@@ -102,7 +128,7 @@ __global__ void __launch_bounds__(128, NMFB_CSC_MINB) csc_linear_v4x_kernel(
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
         const int c = lane + 32 * q;
-        if (c < nq) out[c] = acc[q];
+        if (c < nq) NMFB_STO_(out + c, acc[q]);
     }
 }
 
@@ -115,7 +141,8 @@ template <typename TA, typename TY, int NV>
 __global__ void __launch_bounds__(128, NMFB_CSR_MINB) csr_yt_chunk_v4x_kernel(
     const int64_t *__restrict__ chunks, int64_t nchunks, const int64_t *__restrict__ seg, int nblk,
     int b, const int32_t *__restrict__ colidx, const float *__restrict__ vals,
-    const float *__restrict__ FT, int r, TY *__restrict__ YT, TA *__restrict__ part) {
+    const float *__restrict__ FT, int r, TY *__restrict__ YT, TA *__restrict__ part,
+    bool stream_out) {
     const int64_t ch = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (ch >= nchunks) return;
     const int lane = threadIdx.x & 31;
@@ -143,8 +170,8 @@ __global__ void __launch_bounds__(128, NMFB_CSR_MINB) csr_yt_chunk_v4x_kernel(
         int mycol = 0;
         float myv = 0.f;
         if (lane < cnt) {
-            mycol = colidx[base + lane];
-            myv = vals[base + lane];
+            mycol = NMFB_LDS_(colidx + base + lane);
+            myv = NMFB_LDS_(vals + base + lane);
         }
         if constexpr (sizeof(TY) == 8) {
             // fp64 Y^T (check / blocked passes): every product accumulated in fp64
@@ -205,7 +232,7 @@ __global__ void __launch_bounds__(128, NMFB_CSR_MINB) csr_yt_chunk_v4x_kernel(
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 if (slot < 0)
-                    outy[4 * c + t] = (TY)a[q][t];
+                    NMFB_STO_(outy + 4 * c + t, (TY)a[q][t]);
                 else
                     outp[4 * c + t] = a[q][t];
             }
@@ -260,13 +287,14 @@ int csc_linear_vec_launch(const int64_t *indptr, const int64_t *seg, int nblk,
     if (hi <= lo) return NMFB_OK;
     if (!sparse_vec_ok(r, G, h) || nblk < 1 || (seg && lo != 0)) return NMFB_ERR_ARG;
     const dim3 grid((unsigned)((hi - lo + 3) / 4));
+    const bool so = (hi - lo) * r * (int64_t)sizeof(float) > kStreamOutBytes;
     for (int b = 0; b < (seg ? nblk : 1); ++b) {
         if (r <= 128)
             csc_linear_v4x_kernel<1><<<grid, 128, 0, st>>>(indptr, seg, nblk, b, rowidx, vals, lo,
-                                                           hi, G, r, (float)mu1, h);
+                                                           hi, G, r, (float)mu1, h, so);
         else
             csc_linear_v4x_kernel<2><<<grid, 128, 0, st>>>(indptr, seg, nblk, b, rowidx, vals, lo,
-                                                           hi, G, r, (float)mu1, h);
+                                                           hi, G, r, (float)mu1, h, so);
     }
     return launch_status();
 }
@@ -276,13 +304,15 @@ static int csr_vec_go(const int64_t *chunks, int64_t nchunks, const int64_t *hea
                       const int64_t *seg, int nblk, const int32_t *colidx, const float *vals,
                       const float *FT, int r, TY *YT, double *part, cudaStream_t st) {
     const dim3 grid((unsigned)((nchunks + 3) / 4));
+    // (the chunk count bounds the row count from above)
+    const bool so = nchunks * r * (int64_t)sizeof(TY) > kStreamOutBytes;
     for (int b = 0; b < (seg ? nblk : 1); ++b) {
         if (r <= 128)
             csr_yt_chunk_v4x_kernel<double, TY, 1><<<grid, 128, 0, st>>>(
-                chunks, nchunks, seg, nblk, b, colidx, vals, FT, r, YT, part);
+                chunks, nchunks, seg, nblk, b, colidx, vals, FT, r, YT, part, so);
         else
             csr_yt_chunk_v4x_kernel<double, TY, 2><<<grid, 128, 0, st>>>(
-                chunks, nchunks, seg, nblk, b, colidx, vals, FT, r, YT, part);
+                chunks, nchunks, seg, nblk, b, colidx, vals, FT, r, YT, part, so);
     }
     if (nheavy > 0)
         csr_fold_kernel<double, TY><<<(unsigned)((nheavy + 3) / 4), 128, 0, st>>>(
