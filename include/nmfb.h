@@ -387,6 +387,16 @@ int nmfb_reduce_scatter_panel(void *comm, const void *send, void *recv, int64_t 
 int nmfb_allgather_panel(void *comm, const void *send, void *recv, int64_t send_count, int dtype,
                          void *stream);
 
+/* Row-chunk plan of the load-balanced Y^T pass, built on the device from
+ * the CSR row pointer: row i with k nonzeros -> max(1, ceil(k / chunk))
+ * chunks [4 x int64: row, lo, hi, slot] in row order (slot -1 for single-chunk
+ * rows, else the heavy rows' partial slots numbered consecutively); heavy
+ * rows [3 x int64: row, first slot, count].  Capacities: chunks rows + nnz /
+ * chunk + 1 entries, heavy rows entries.  counts_out (HOST int64[3]): number
+ * of chunks, heavy rows, slots (synchronises the stream). */
+int nmfb_csr_chunk_plan(const int64_t *rowptr, int64_t rows, int64_t chunk, int64_t *chunks,
+                        int64_t *heavy, int64_t *counts_out, void *stream);
+
 /* Return the ingest kernels' cached scratch (a private stream-ordered pool on
  * the current device, kept mapped between ingests) to the driver.  Waits for
  * the device. */

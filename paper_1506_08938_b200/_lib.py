@@ -104,6 +104,7 @@ SIGNATURES = {
     "nmfb_csc_to_csr": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
     "nmfb_csc_validate": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp, _vp]),
     "nmfb_ingest_release_scratch": (_int, []),
+    "nmfb_csr_chunk_plan": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "nmfb_comm_available": (_int, []),
     "nmfb_comm_unique_id": (_int, [_vp]),
     "nmfb_comm_init": (_int, [_vp, _i32, _i32, _vp]),
@@ -183,7 +184,7 @@ KERNELS_PER_CALL = {
     "nmfb_tc_gemm_rows": 1, "nmfb_nnls_batch_peers": 1, "nmfb_peer_put": 1, "nmfb_peer_wait": 1,
     "nmfb_sum_slots_f64": 1, "nmfb_csc_from_triplets": 11, "nmfb_csc_to_csr": 8,
     "nmfb_csc_validate": 2, "nmfb_narrow_indices": 2, "nmfb_mur_update": 1,
-    "nmfb_ingest_release_scratch": 0, "nmfb_comm_available": 0, "nmfb_comm_unique_id": 0,
+    "nmfb_ingest_release_scratch": 0, "nmfb_csr_chunk_plan": 5, "nmfb_comm_available": 0, "nmfb_comm_unique_id": 0,
     "nmfb_comm_init": 0, "nmfb_comm_destroy": 0, "nmfb_allreduce_r2": 1,
     "nmfb_reduce_scatter_panel": 1, "nmfb_allgather_panel": 1,
     "nmfb_init_factors": 1, "nmfb_csc_segments": 1, "nmfb_chunk_segments": 1, "nmfb_sum_slots_rescale": 1,

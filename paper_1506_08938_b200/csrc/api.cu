@@ -39,6 +39,8 @@ int csc_validate_launch(int64_t rows, int64_t cols, int64_t nnz, const int64_t *
                         const int32_t *rowidx, const void *vals, int vals_dtype, int64_t *info,
                         cudaStream_t st);
 int ingest_release_scratch();
+int csr_chunk_plan_launch(const int64_t *rowptr, int64_t rows, int64_t chunk, int64_t *chunks,
+                          int64_t *heavy, int64_t *counts_out, cudaStream_t st);
 int comm_available();
 int comm_unique_id(void *id);
 int comm_init(const void *id, int rank, int nranks, void **comm);
@@ -498,6 +500,12 @@ int nmfb_csc_validate(int64_t rows, int64_t cols, int64_t nnz, const int64_t *in
 }
 
 int nmfb_ingest_release_scratch(void) { return check(ingest_release_scratch()); }
+
+int nmfb_csr_chunk_plan(const int64_t *rowptr, int64_t rows, int64_t chunk, int64_t *chunks,
+                        int64_t *heavy, int64_t *counts_out, void *stream) {
+    return check(csr_chunk_plan_launch(rowptr, rows, chunk, chunks, heavy, counts_out,
+                                       (cudaStream_t)stream));
+}
 
 int nmfb_comm_available(void) { return comm_available(); }
 int nmfb_comm_unique_id(void *id_out) { return check(comm_unique_id(id_out)); }

@@ -392,6 +392,87 @@ __global__ void narrow_kernel(const int64_t *__restrict__ in, int64_t n, int32_t
     }
 }
 
+// ---------------------------------------------------------------------------
+// Row-chunk plan of the load-balanced Y^T pass (paper_1506_08938_b200/device.py
+// csr_chunk_plan, same definition): row i with k nonzeros -> max(1,
+// ceil(k / chunk)) chunks (row, lo, hi, slot); rows with more than one chunk
+// ("heavy") number their chunks' partial slots consecutively in row order and
+// get an entry (row, first slot, count).  counts_out (host int64[3]): total
+// chunks, heavy rows, slots.  chunks_out capacity: rows + nnz / chunk + 1;
+// heavy_out capacity: rows.
+// ---------------------------------------------------------------------------
+__global__ void chunk_counts_kernel(const int64_t *__restrict__ rowptr, int64_t rows, int64_t chunk,
+                                    int64_t *nch, int64_t *hch, int64_t *hflag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = rowptr[i + 1] - rowptr[i];
+        int64_t c = (k + chunk - 1) / chunk;
+        if (c < 1) c = 1;
+        nch[i] = c;
+        hch[i] = c > 1 ? c : 0;
+        hflag[i] = c > 1 ? 1 : 0;
+    }
+}
+
+__global__ void chunk_fill_kernel(const int64_t *__restrict__ rowptr, int64_t rows, int64_t chunk,
+                                  const int64_t *__restrict__ nch, const int64_t *__restrict__ first,
+                                  const int64_t *__restrict__ hfirst,
+                                  const int64_t *__restrict__ hidx, int64_t *chunks,
+                                  int64_t *heavy) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = nch[i], f = first[i], p0 = rowptr[i], p1 = rowptr[i + 1];
+        const bool hv = c > 1;
+        for (int64_t q = 0; q < c; ++q) {
+            const int64_t lo = p0 + q * chunk;
+            int64_t *o = chunks + 4 * (f + q);
+            o[0] = i;
+            o[1] = lo;
+            o[2] = lo + chunk < p1 ? lo + chunk : p1;
+            o[3] = hv ? hfirst[i] + q : -1;
+        }
+        if (hv) {
+            int64_t *h = heavy + 3 * hidx[i];
+            h[0] = i;
+            h[1] = hfirst[i];
+            h[2] = c;
+        }
+    }
+}
+
+int csr_chunk_plan_launch(const int64_t *rowptr, int64_t rows, int64_t chunk, int64_t *chunks,
+                          int64_t *heavy, int64_t *counts_out, cudaStream_t st) {
+    if (rows <= 0 || chunk <= 0 || !rowptr || !chunks || !heavy || !counts_out)
+        return NMFB_ERR_ARG;
+    Pool pool(st);
+    int64_t *nch = pool.get<int64_t>(rows), *hch = pool.get<int64_t>(rows);
+    int64_t *hflag = pool.get<int64_t>(rows), *first = pool.get<int64_t>(rows);
+    int64_t *hfirst = pool.get<int64_t>(rows), *hidx = pool.get<int64_t>(rows);
+    int64_t *tail = pool.get<int64_t>(6);
+    if (!nch || !hch || !hflag || !first || !hfirst || !hidx || !tail) return NMFB_ERR_CUDA;
+    const unsigned grid = grid_for(rows);
+    chunk_counts_kernel<<<grid, TB, 0, st>>>(rowptr, rows, chunk, nch, hch, hflag);
+    int rc = exclusive_sum(pool, nch, first, rows);
+    if (!rc) rc = exclusive_sum(pool, hch, hfirst, rows);
+    if (!rc) rc = exclusive_sum(pool, hflag, hidx, rows);
+    if (rc) return rc;
+    chunk_fill_kernel<<<grid, TB, 0, st>>>(rowptr, rows, chunk, nch, first, hfirst, hidx, chunks,
+                                           heavy);
+    // totals = last exclusive prefix + last count
+    const int64_t *src[6] = {first + rows - 1, nch + rows - 1, hidx + rows - 1,
+                             hflag + rows - 1, hfirst + rows - 1, hch + rows - 1};
+    for (int k = 0; k < 6; ++k)
+        cudaMemcpyAsync(tail + k, src[k], sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    int64_t h[6];
+    if (cudaMemcpyAsync(h, tail, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return NMFB_ERR_CUDA;
+    counts_out[0] = h[0] + h[1];
+    counts_out[1] = h[2] + h[3];
+    counts_out[2] = h[4] + h[5];
+    return launch_status();
+}
+
 int ingest_release_scratch() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return NMFB_ERR_CUDA;

@@ -124,6 +124,22 @@ def csr_chunk_plan(rowptr, chunk=CSR_CHUNK):
     return np.ascontiguousarray(chunks), np.ascontiguousarray(heavy), int(in_heavy.sum())
 
 
+def device_chunk_plan(rowptr, n, nnz, device, chunk=CSR_CHUNK):
+    """csr_chunk_plan built on the device (nmfb_csr_chunk_plan): the same
+    (chunks, heavy) tables as device tensors, plus the slot count."""
+    import ctypes
+
+    cap = n + nnz // chunk + 1
+    chunks = torch.empty((max(cap, 1), 4), dtype=torch.int64, device=device)
+    heavy = torch.empty((max(n, 1), 3), dtype=torch.int64, device=device)
+    counts = np.zeros(3, dtype=np.int64)
+    if n == 0:
+        return chunks[:0], heavy[:0], 0
+    L.call("nmfb_csr_chunk_plan", vp(rowptr), n, chunk, vp(chunks), vp(heavy),
+           counts.ctypes.data_as(ctypes.c_void_p), stream_handle())
+    return chunks[: int(counts[0])], heavy[: int(counts[1])], int(counts[2])
+
+
 def shard_bounds(total, workers):
     shards = block_plan(total, workers)
     return [shards[0][0]] + [hi for _, hi in shards]
@@ -296,10 +312,9 @@ class DeviceData:
             self.indptr, self.rowidx, self.vals = csc.indptr, csc.rowidx, csc.values
             self.rowptr, self.colidx, self.cvals = csc.csr()
             # the row-chunk plan of the load-balanced Y^T pass: O(n) on the host
-            chunks, heavy, nslots = csr_chunk_plan(self.rowptr.cpu().numpy())
-            self.chunks = torch.from_numpy(chunks).to(self.device)
-            self.heavy = torch.from_numpy(heavy).to(self.device)
-            self.nchunks, self.nheavy, self.nslots = len(chunks), len(heavy), nslots
+            self.chunks, self.heavy, self.nslots = device_chunk_plan(self.rowptr, self.n,
+                                                                     V.nnz, self.device)
+            self.nchunks, self.nheavy = len(self.chunks), len(self.heavy)
             self.nnz = V.nnz
             self.host = V if isinstance(V, SparseMatrix) else None
             self.csc = csc

@@ -127,3 +127,24 @@ def test_gram_side_stream_overlap_bit_identical(monkeypatch):
     assert np.array_equal(m0.G.array, m1.G.array)
     assert np.array_equal(m0.F.array, m1.F.array)
     assert l0.objective == l1.objective
+
+
+def test_device_chunk_plan_equals_host_plan():
+    """nmfb_csr_chunk_plan builds exactly device.csr_chunk_plan's tables."""
+    import torch
+
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    rng = np.random.default_rng(12)
+    for n, chunk in ((1, 256), (5000, 256), (3000, 7), (20000, 64)):
+        k = np.minimum(rng.zipf(1.3, size=n) - 1, 3000)
+        k[rng.random(n) < 0.1] = 0  # empty rows
+        rowptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(k, out=rowptr[1:])
+        hc, hh, hs = D.csr_chunk_plan(rowptr, chunk=chunk)
+        dc, dh, ds = D.device_chunk_plan(torch.from_numpy(rowptr).to(dev), n, int(rowptr[-1]),
+                                         dev, chunk=chunk)
+        assert ds == hs
+        assert np.array_equal(dc.cpu().numpy(), hc)
+        assert np.array_equal(dh.cpu().numpy().reshape(-1, 3), hh.reshape(-1, 3))
