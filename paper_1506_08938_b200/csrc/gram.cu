@@ -130,6 +130,11 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double *__restri
     }
 }
 
+// tensor-core partials for fp32 factors (gram_tc.cu)
+bool gram_tc_ok(const void *A, int64_t rows, int r, int64_t lda);
+int gram_tc_partial_launch(const float *A, int64_t rows, int r, int64_t lda, double *part,
+                           int64_t *nunit, cudaStream_t st);
+
 static int64_t gram_chunk(int64_t rows) {
     // ~2 chunks per SM (148 SMs), each a whole number of GROWS-row slabs; the
     // reduce is parallel over entries, so many chunks cost little
@@ -160,6 +165,9 @@ int gram_launch(int dtype, const void *A, int64_t rows, int r, int64_t lda, doub
     dim3 grid(ntile * (ntile + 1) / 2, (unsigned)nchunk);
     if (rows == 0) {
         cudaMemsetAsync(part, 0, sizeof(double) * r * r, st);
+    } else if (dtype == NMFB_F32 && gram_tc_ok(A, rows, r, lda)) {
+        int rc = gram_tc_partial_launch((const float *)A, rows, r, lda, part, &nchunk, st);
+        if (rc != NMFB_OK) return rc;
     } else if (dtype == NMFB_F64) {
         gram_partial_kernel<double><<<grid, 256, 0, st>>>((const double *)A, rows, r, lda, chunk,
                                                           part);
@@ -306,13 +314,17 @@ int gram_rescale_launch(int dtype, const void *A, int64_t rows, int r, int64_t l
     int64_t chunk = gram_chunk(rows);
     int64_t nchunk = rows > 0 ? (rows + chunk - 1) / chunk : 1;
     double *part = (double *)ws;
-    unsigned *ticket = (unsigned *)((char *)ws + (size_t)nchunk * r * r * sizeof(double));
+    // the ticket sits past the largest partial area this workspace can hold
+    unsigned *ticket = (unsigned *)((char *)ws + gram_workspace_bytes(rows, r) - 64);
     cudaMemsetAsync(ticket, 0, sizeof(unsigned), st);
     int ntile = (r + GT - 1) / GT;
     dim3 grid(ntile * (ntile + 1) / 2, (unsigned)nchunk);
-    if (rows == 0)
+    if (rows == 0) {
         cudaMemsetAsync(part, 0, sizeof(double) * r * r, st);
-    else if (dtype == NMFB_F64)
+    } else if (dtype == NMFB_F32 && gram_tc_ok(A, rows, r, lda)) {
+        int rc = gram_tc_partial_launch((const float *)A, rows, r, lda, part, &nchunk, st);
+        if (rc != NMFB_OK) return rc;
+    } else if (dtype == NMFB_F64)
         gram_partial_kernel<double><<<grid, 256, 0, st>>>((const double *)A, rows, r, lda, chunk,
                                                           part);
     else
