@@ -81,7 +81,11 @@ __global__ void __maxnreg__(128)
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t half_bytes = (uint32_t)NB * GTC_BOX_BYTES;  // hi (or lo) tile of a stage
     const uint32_t stage_bytes = 2 * half_bytes;
-    uint64_t *bars = (uint64_t *)(smem + (size_t)stages * stage_bytes);
+    // r <= 96: the M = 128 operand reads 4 - NB atom columns past a tile (they
+    // feed accumulator rows >= 32 NB, never stored); the last stage's overrun
+    // lands in this pad, inside the allocation
+    const uint32_t pad_bytes = NB < 4 ? (uint32_t)(4 - NB) * GTC_BOX_BYTES : 0u;
+    uint64_t *bars = (uint64_t *)(smem + (size_t)stages * stage_bytes + pad_bytes);
     uint64_t *full = bars, *split_done = bars + stages, *empty = bars + 2 * stages;
     uint64_t *d_full = bars + 3 * stages;       // [2]
     uint64_t *d_empty = bars + 3 * stages + 2;  // [2]
@@ -392,11 +396,12 @@ int gram_tc_partial_launch(const float *A, int64_t rows, int r, int64_t lda, dou
             return NMFB_ERR_ARG;
     }
     const size_t stage_bytes = 2 * (size_t)NB * GTC_BOX_BYTES;
-    const size_t budget = 227 * 1024 - 1024 - 512;
+    const size_t pad_bytes = NB < 4 ? (size_t)(4 - NB) * GTC_BOX_BYTES : 0;
+    const size_t budget = 227 * 1024 - 1024 - 512 - pad_bytes;
     int stages = (int)(budget / stage_bytes);
     if (stages > 8) stages = 8;
     if (stages < 3) return NMFB_ERR_ARG;
-    const size_t smem = stages * stage_bytes + (3 * stages + 6) * 8 + 1024;
+    const size_t smem = stages * stage_bytes + pad_bytes + (3 * stages + 6) * 8 + 1024;
     // per device, cheap: set on every call
     if (cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024) != cudaSuccess)

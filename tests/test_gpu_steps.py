@@ -196,3 +196,49 @@ def test_gram_against_oracle_and_exact(rows, r):
     rel = [abs(g32[i, j] - math.fsum(A32[:, i] * A32[:, j])) / abs(math.fsum(A32[:, i] * A32[:, j]))
            for i, j in pairs]
     assert max(rel) < 1e-6, max(rel)
+
+
+@pytest.mark.parametrize("rows,r,pad", [(2048, 16, 0), (4097, 32, 0), (30001, 64, 4), (9999, 100, 0),
+                                        (5000, 128, 0), (7777, 132, 0), (20000, 160, 8),
+                                        (70000, 200, 0), (30001, 224, 0)])
+def test_gram_tensor_core_path(rows, r, pad):
+    """The tcgen05 Gram (csrc/gram_tc.cu: fp32 factors, r % 4 == 0, r <= 224,
+    rows >= 2048; matrix.py:181-197) against the exact Gram of the same fp32
+    values (fp64 matmul of exactly representable products).  3xTF32 products
+    and 64-row chunks promoted into round-to-nearest running sums: within 1e-6
+    relative on every entry (measured 4.6e-7, almost all of it a uniform
+    -4.0e-7 bias of the truncating tensor-core accumulate, which the unit-
+    diagonal rescale cancels), exactly symmetric, and the same through a padded
+    leading dimension and with a ragged last unit.  NMFB_GRAM_TC=0 in the
+    environment selects the CUDA-core kernel (this test then checks that)."""
+    import torch
+
+    from paper_1506_08938_b200 import _lib as L
+    from paper_1506_08938_b200 import device as D
+
+    dev = D.require_cuda()
+    g = torch.Generator(device="cpu").manual_seed(rows * 31 + r)
+    A = torch.rand((rows, r + pad), generator=g) ** 3 * (torch.rand((1, r + pad), generator=g) * 10
+                                                         + 0.01)
+    A[:, r // 2] *= (torch.rand(rows, generator=g) < 0.05)  # a sparse factor column
+    A[:, 1] = 0.0                                           # a dead one
+    a = A.to(dev, torch.float32)
+    out = torch.zeros((r, r), dtype=torch.float64, device=dev)
+    ws = torch.full((L.lib().nmfb_gram_workspace_bytes(rows, r) // 8 + 1,), float("nan"),
+                    dtype=torch.float64, device=dev)
+    L.call("nmfb_gram", L.F32, D.vp(a), rows, r, r + pad, D.vp(out), D.vp(ws), D.stream_handle())
+    torch.cuda.synchronize()
+    a64 = a[:, :r].double()
+    want = a64.T @ a64
+    assert torch.equal(out, out.T)
+    assert torch.isfinite(out).all()
+    assert torch.equal(out[1], torch.zeros_like(out[1]))
+    rel = ((out - want).abs() / want.abs().clamp_min(1e-300))[want != 0]
+    assert rel.max().item() < 1e-6, rel.max().item()
+    # the rescaled Q (what the NNLS reads, nqp.py:116-131) is insensitive to the
+    # uniform part of the error
+    keep = [i for i in range(r) if i != 1]
+    d = torch.sqrt(torch.diagonal(out)[keep]); dw = torch.sqrt(torch.diagonal(want)[keep])
+    q = out[keep][:, keep] / (d[:, None] * d[None, :])
+    qw = want[keep][:, keep] / (dw[:, None] * dw[None, :])
+    assert (q - qw).abs().max().item() < 2e-7, (q - qw).abs().max().item()
