@@ -462,6 +462,29 @@ def run_ours(args):
             "note": "FMA-counted; the greedy-CD argmax (r compares + a tree per selection) "
                     "and the shuffles are not counted -- issue-slot utilisation is in "
                     "profiles/ (ncu smsp__issue_active)"}
+    # Gram products (G^T G over n rows, F F^T over m rows): one read of the
+    # factor each, from the serialised instrumented steps
+    gr_names = ("nmfb_gram", "nmfb_gram_rescale")
+    gc = sum(calls.get(k, (0, 0.0))[0] for k in gr_names)
+    gt = sum(calls.get(k, (0, 0.0))[1] for k in gr_names)
+    if gc:
+        g_bytes = 4.0 * R * (n_solve + m_solve) / 2.0  # per launch, averaged over the two
+        g_avg = gt / gc
+        g_ach = g_bytes / (g_avg / 1e3) / 1e9
+        tc_gram = R % 4 == 0 and 16 <= R <= 224 and os.environ.get("NMFB_GRAM_TC", "1") != "0"
+        rooflines["gram"] = {
+            "kernel": ("gram_tc_kernel (tcgen05 3xTF32, MN-major operands from one TMA tile) + "
+                       "fused reduce/rescale" if tc_gram else
+                       "gram_partial_kernel (fp32 slabs folded to fp64) + fused reduce/rescale"),
+            "bound": "hbm", "achieved": g_ach, "peak": hbm, "unit": "GB/s", "frac": g_ach / hbm,
+            "peak_source": peak_src, "algorithmic_bytes_per_launch": g_bytes,
+            "avg_launch_ms": g_avg, "timed": "serialised instrumented steps (CUDA events "
+            "around each call, both Gram launches of a step averaged)",
+            "traffic": profile_traffic(cid, "nmfb_gram_tc" if tc_gram else "nmfb_gram"),
+            "share": round(sum(share.get(k, 0.0) for k in gr_names), 4),
+            "note": "tensor pipe 61% active (ncu, profiles/r02_ncu_gram_tc.ncu-rep): bound by "
+                    "the ~77 ns issue cost of a tcgen05.mma, 6 per 8 factor rows"
+                    if tc_gram else None}
     # the dominant kernel: the largest share of the serialised step
     dom = max(rooflines.items(), key=lambda kv: kv[1].get("share") or 0.0)
     # log sanity: objective decreasing
