@@ -230,18 +230,34 @@ __device__ void rescale_body(const double *__restrict__ G, int r, double diag_ad
         if (full_scale) full_scale[i] = sq[i];
         if (pos[i] >= 0) scale_a[pos[i]] = (T)sq[i];
     }
-    for (int idx = tid; idx < r * r; idx += blockDim.x) {
-        int i = idx / r, j = idx % r;
-        int pi = pos[i], pj = pos[j];
-        if (pi < 0 || pj < 0) continue;
-        double v;
-        if (i == j) {
-            v = 1.0;
-        } else {
-            // off-diagonal of H = G + diag_add * eye: G_ij + 0.0
-            v = __ddiv_rn(__dadd_rn(__ldcg(G + i * r + j), 0.0), __dmul_rn(sq[i], sq[j]));
+    // eight entries per thread per pass: the L2 loads of a pass are issued
+    // together (a load -> divide -> store chain per entry left one load in
+    // flight per thread: ~65 us at r = 200)
+    constexpr int U = 8;
+    const int step = (int)blockDim.x;
+    for (int base = tid; base < r * r; base += U * step) {
+        double g[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int idx = base + u * step;
+            g[u] = idx < r * r ? __ldcg(G + idx) : 0.0;
         }
-        Qa[pi * ra + pj] = (T)v;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int idx = base + u * step;
+            if (idx >= r * r) continue;
+            const int i = idx / r, j = idx - i * r;
+            const int pi = pos[i], pj = pos[j];
+            if (pi < 0 || pj < 0) continue;
+            double v;
+            if (i == j) {
+                v = 1.0;
+            } else {
+                // off-diagonal of H = G + diag_add * eye: G_ij + 0.0
+                v = __ddiv_rn(__dadd_rn(g[u], 0.0), __dmul_rn(sq[i], sq[j]));
+            }
+            Qa[pi * ra + pj] = (T)v;
+        }
     }
 }
 

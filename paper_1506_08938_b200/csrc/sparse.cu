@@ -376,10 +376,26 @@ __global__ void csr_yt_fold_kernel(const int64_t *__restrict__ heavy, int64_t nh
     if (h >= nheavy) return;
     const int lane = threadIdx.x & 31;
     const int64_t row = heavy[h * 3 + 0], first = heavy[h * 3 + 1], count = heavy[h * 3 + 2];
-    for (int i = lane; i < r; i += 32) {
-        TY s = TY(0);
-        for (int64_t k = 0; k < count; ++k) s += part[(first + k) * r + i];
-        YT[row * r + i] = s;
+    // same per-element slot order as a plain loop (0 + p0 + p1 + ...), with
+    // eight elements per lane and four slots unrolled so the loads overlap
+    for (int i0 = 0; i0 < r; i0 += 256) {
+        TY s[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] = TY(0);
+#pragma unroll 4
+        for (int64_t k = 0; k < count; ++k) {
+            const TY *p = part + (first + k) * r;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + lane + 32 * q;
+                if (i < r) s[q] += p[i];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int i = i0 + lane + 32 * q;
+            if (i < r) YT[row * r + i] = s[q];
+        }
     }
 }
 

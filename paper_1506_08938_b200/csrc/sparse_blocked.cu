@@ -247,10 +247,48 @@ __global__ void csr_fold_kernel(const int64_t *__restrict__ heavy, int64_t nheav
     if (hv >= nheavy) return;
     const int lane = threadIdx.x & 31;
     const int64_t row = heavy[hv * 3 + 0], s0 = heavy[hv * 3 + 1], ns = heavy[hv * 3 + 2];
-    for (int i = lane; i < r; i += 32) {
-        TA s = part[s0 * r + i];
-        for (int64_t k = 1; k < ns; ++k) s += part[(s0 + k) * r + i];
-        YT[row * r + i] = (TY)s;
+    // slots summed in slot order per element (deterministic); eight elements
+    // per lane and four slots unrolled keep ~32 independent loads in flight
+    // instead of one dependent load per slot
+    for (int i0 = 0; i0 < r; i0 += 256) {
+        TA s[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int i = i0 + lane + 32 * q;
+            s[q] = i < r ? part[s0 * r + i] : TA(0);
+        }
+        int64_t k = 1;
+        for (; k + 4 <= ns; k += 4) {
+            // all 32 loads issued before the first add consumes one
+            TA v[4][8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = i0 + lane + 32 * q;
+                    v[u][q] = i < r ? __ldg(part + (s0 + k + u) * r + i) : TA(0);
+                }
+            asm volatile("" ::: "memory");  // keep the loads ahead of the adds
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s[q] += v[u][q];
+        }
+        for (; k < ns; ++k) {
+            TA v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + lane + 32 * q;
+                v[q] = i < r ? __ldg(part + (s0 + k) * r + i) : TA(0);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s[q] += v[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int i = i0 + lane + 32 * q;
+            if (i < r) YT[row * r + i] = (TY)s[q];
+        }
     }
 }
 
