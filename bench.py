@@ -574,6 +574,10 @@ def run_e2e(args, X, cfg):
     wcfg = NmfConfig(max_outer=2, rel_change_tol=0.0, precision="fp32", **knobs)
 
     def timed(V):
+        # two short warm-up fits: the allocator's block cache, the pinned
+        # staging buffers and the ingest scratch pool only settle during the
+        # second call of a process (its fit is ~60 ms slower at C5)
+        fit(V, wcfg)
         fit(V, wcfg)
         torch.cuda.synchronize()
         t = time.perf_counter()

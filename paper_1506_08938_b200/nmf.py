@@ -23,7 +23,7 @@ import torch
 from . import device as D
 from .ingest import DeviceCsc
 from .exceptions import NumericalFailureError
-from .matrix import (DenseMatrix, SparseMatrix, frobenius_objective, require_nonnegative,
+from .matrix import (DenseMatrix, SparseMatrix, exact_sum, frobenius_objective, require_nonnegative,
                      sparse_col_times_dense)
 from .nqp import DEFAULT_EPSILON, DEFAULT_MAX_INNER, NqpProblem
 
@@ -115,7 +115,8 @@ def _shape(V):
 def _mean(V):
     """nmf.py:109-112."""
     n, m = _shape(V)
-    total = float(np.sum(V.values)) if isinstance(V, SparseMatrix) else float(np.sum(V.array))
+    # np.sum's value bit for bit; long sparse value vectors on worker threads
+    total = exact_sum(V.values) if isinstance(V, SparseMatrix) else float(np.sum(V.array))
     return total / (n * m)
 
 
