@@ -444,15 +444,6 @@ int nmfb_chunk_segments(const int64_t *chunks, int64_t nchunks, const int32_t *c
 int nmfb_csc_linear_blocked(const int64_t *indptr, const int64_t *seg, int32_t nblk,
                             const int32_t *rowidx, const float *vals, int64_t m, const float *G,
                             int32_t r, double mu1, float *h, void *stream);
-/* Passes [b_lo, b_hi) of nmfb_csc_linear_blocked only.  Pass b reads just the
- * rows of G in block b ([b * blk, (b + 1) * blk)), so a caller may launch the
- * passes in increasing b as soon as those rows are final -- the single-GPU fit
- * overlaps the next iteration's G^T X with the component step's row panels
- * this way (kernels.py:251-258 for the following outer iteration). */
-int nmfb_csc_linear_blocked_range(const int64_t *indptr, const int64_t *seg, int32_t nblk,
-                                  int32_t b_lo, int32_t b_hi, const int32_t *rowidx,
-                                  const float *vals, int64_t m, const float *G, int32_t r,
-                                  double mu1, float *h, void *stream);
 int nmfb_csr_yt_chunked_blocked(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
                                 int64_t nheavy, const int64_t *seg, int32_t nblk,
                                 const int32_t *colidx, const float *vals, const float *FT,

@@ -119,8 +119,6 @@ SIGNATURES = {
     "nmfb_chunk_segments": (_int, [_vp, _i64, _vp, _i64, _i32, _vp, _vp]),
     "nmfb_csc_linear_blocked": (_int, [_vp, _vp, _i32, _vp, _vp, _i64, _vp, _i32, _f64, _vp,
                                        _vp]),
-    "nmfb_csc_linear_blocked_range": (_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i64, _vp,
-                                             _i32, _f64, _vp, _vp]),
     "nmfb_csr_yt_chunked_blocked": (_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _vp, _vp, _i32,
                                            _int, _vp, _vp, _vp]),
     "nmfb_init_factors": (_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
@@ -191,7 +189,6 @@ KERNELS_PER_CALL = {
     "nmfb_reduce_scatter_panel": 1, "nmfb_allgather_panel": 1,
     "nmfb_init_factors": 1, "nmfb_csc_segments": 1, "nmfb_chunk_segments": 1, "nmfb_sum_slots_rescale": 1,
     "nmfb_csc_linear_blocked": 1, "nmfb_csr_yt_chunked_blocked": 2,
-    "nmfb_csc_linear_blocked_range": 1,
 }
 
 

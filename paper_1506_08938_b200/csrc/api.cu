@@ -18,10 +18,6 @@ int chunk_segments_launch(const int64_t *chunks, int64_t nchunks, const int32_t 
 int csc_linear_vec_launch(const int64_t *indptr, const int64_t *seg, int nblk,
                           const int32_t *rowidx, const float *vals, int64_t lo, int64_t hi,
                           const float *G, int r, double mu1, float *h, cudaStream_t st);
-int csc_linear_vec_range_launch(const int64_t *indptr, const int64_t *seg, int nblk, int b_lo,
-                                int b_hi, const int32_t *rowidx, const float *vals, int64_t lo,
-                                int64_t hi, const float *G, int r, double mu1, float *h,
-                                cudaStream_t st);
 int csr_yt_chunked_vec_launch(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,
                               int64_t nheavy, const int64_t *seg, int nblk, const int32_t *colidx,
                               const float *vals, const float *FT, int r, int yt_dtype, void *YT,
@@ -455,15 +451,6 @@ int nmfb_csc_linear_blocked(const int64_t *indptr, const int64_t *seg, int32_t n
                             int32_t r, double mu1, float *h, void *stream) {
     return check(csc_linear_vec_launch(indptr, seg, nblk, rowidx, vals, 0, m, G, r, mu1, h,
                                        (cudaStream_t)stream));
-}
-
-int nmfb_csc_linear_blocked_range(const int64_t *indptr, const int64_t *seg, int32_t nblk,
-                                  int32_t b_lo, int32_t b_hi, const int32_t *rowidx,
-                                  const float *vals, int64_t m, const float *G, int32_t r,
-                                  double mu1, float *h, void *stream) {
-    if (!seg) return check(NMFB_ERR_ARG);
-    return check(csc_linear_vec_range_launch(indptr, seg, nblk, b_lo, b_hi, rowidx, vals, 0, m, G,
-                                             r, mu1, h, (cudaStream_t)stream));
 }
 
 int nmfb_csr_yt_chunked_blocked(const int64_t *chunks, int64_t nchunks, const int64_t *heavy,

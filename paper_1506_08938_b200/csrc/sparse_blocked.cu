@@ -301,11 +301,6 @@ inline bool vec_ok(int r, const void *a) {
 // true when the vectorised kernels below apply (fp32 data, r % 4 == 0, r <= 256)
 bool sparse_vec_ok(int r, const void *a, const void *b) { return vec_ok(r, a) && vec_ok(r, b); }
 
-int csc_linear_vec_range_launch(const int64_t *indptr, const int64_t *seg, int nblk, int b_lo,
-                                int b_hi, const int32_t *rowidx, const float *vals, int64_t lo,
-                                int64_t hi, const float *G, int r, double mu1, float *h,
-                                cudaStream_t st);
-
 int csc_segments_launch(const int64_t *indptr, const int32_t *rowidx, int64_t m, int64_t blk,
                         int nblk, int64_t *seg, cudaStream_t st) {
     if (m <= 0) return NMFB_OK;
@@ -327,23 +322,11 @@ int chunk_segments_launch(const int64_t *chunks, int64_t nchunks, const int32_t 
 int csc_linear_vec_launch(const int64_t *indptr, const int64_t *seg, int nblk,
                           const int32_t *rowidx, const float *vals, int64_t lo, int64_t hi,
                           const float *G, int r, double mu1, float *h, cudaStream_t st) {
-    return csc_linear_vec_range_launch(indptr, seg, nblk, 0, seg ? nblk : 1, rowidx, vals, lo, hi,
-                                       G, r, mu1, h, st);
-}
-
-// Passes [b_lo, b_hi) of the blocked product (pass b gathers only from row
-// block b of G and carries the running sums through h, so the passes may be
-// launched one by one as the rows of G become final -- in increasing b).
-int csc_linear_vec_range_launch(const int64_t *indptr, const int64_t *seg, int nblk, int b_lo,
-                                int b_hi, const int32_t *rowidx, const float *vals, int64_t lo,
-                                int64_t hi, const float *G, int r, double mu1, float *h,
-                                cudaStream_t st) {
     if (hi <= lo) return NMFB_OK;
     if (!sparse_vec_ok(r, G, h) || nblk < 1 || (seg && lo != 0)) return NMFB_ERR_ARG;
-    if (b_lo < 0 || b_hi > (seg ? nblk : 1) || b_lo > b_hi) return NMFB_ERR_ARG;
     const dim3 grid((unsigned)((hi - lo + 3) / 4));
     const bool so = (hi - lo) * r * (int64_t)sizeof(float) > kStreamOutBytes;
-    for (int b = b_lo; b < b_hi; ++b) {
+    for (int b = 0; b < (seg ? nblk : 1); ++b) {
         if (r <= 128)
             csc_linear_v4x_kernel<1><<<grid, 128, 0, st>>>(indptr, seg, nblk, b, rowidx, vals, lo,
                                                            hi, G, r, (float)mu1, h, so);

@@ -9,8 +9,8 @@ from paper_1506_08938_b200.exceptions import DataDomainError
 from paper_1506_08938_b200.matrix import DenseMatrix, SparseMatrix, exact_sum, require_nonnegative
 
 
-@pytest.mark.parametrize("n", [0, 1, 7, 129, 4096, (1 << 22) - 3, 1 << 22, (1 << 22) + 1,
-                               5_000_003, 9_437_189])
+@pytest.mark.parametrize("n", [0, 1, 7, 129, 4096, M._PAR_MIN_SIZE - 3, M._PAR_MIN_SIZE,
+                               M._PAR_MIN_SIZE + 1, 17_000_003, 19_437_189])
 def test_exact_sum_is_numpy_sum_bit_for_bit(n):
     """exact_sum evaluates np.sum's own pairwise tree on worker threads: the
     seeded init scale (nmf.py:115-127) must be the reference's number exactly."""
@@ -53,8 +53,8 @@ def test_require_nonnegative_matches_reference(size, bad, msg):
 
 def test_require_nonnegative_fortran_ordered_dense():
     rng = np.random.default_rng(5)
-    a = np.asfortranarray(rng.random((2100, 2100)))
+    a = np.asfortranarray(rng.random((4100, 4100)))
     require_nonnegative(DenseMatrix(a), "data matrix")
-    a[2099, 17] = -1.0
+    a[4099, 17] = -1.0
     with pytest.raises(DataDomainError, match="negative entries"):
         require_nonnegative(DenseMatrix(a), "data matrix")
