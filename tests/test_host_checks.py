@@ -58,3 +58,13 @@ def test_require_nonnegative_fortran_ordered_dense():
     a[4099, 17] = -1.0
     with pytest.raises(DataDomainError, match="negative entries"):
         require_nonnegative(DenseMatrix(a), "data matrix")
+
+
+def test_exact_sum_falls_back_when_the_tree_does_not_match(monkeypatch):
+    """The one-time self-check: if this numpy's reduction were not the restated
+    pairwise tree, exact_sum must return np.sum's number anyway."""
+    a = np.random.default_rng(3).random(M._PAR_MIN_SIZE + 10_000)
+    monkeypatch.setattr(M, "_EXACT_SUM_OK", None)
+    monkeypatch.setattr(M, "_tree_sum", lambda v: float(np.sum(v)) + 1.0)  # a wrong tree
+    assert exact_sum(a) == float(np.sum(a))
+    assert M._EXACT_SUM_OK is False
