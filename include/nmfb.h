@@ -147,9 +147,15 @@ int nmfb_nqp_solve(const double *Qa, const double *scale_a, const int32_t *act_i
 int nmfb_nqp_step(int32_t op, const double *Q, int32_t r, const double *x, const double *grad,
                   int64_t count, int32_t sweeps, double *x_out, double *grad_out, void *stream);
 
-/* Gram A^T A of A (rows, r) row-major (leading dim lda), accumulated in fp64
- * with a fixed (deterministic) summation order; out = full symmetric r x r
- * fp64.  workspace: nmfb_gram_workspace_bytes(rows, r) bytes of device mem. */
+/* Gram A^T A of A (rows, r) row-major (leading dim lda) with a fixed
+ * (deterministic) summation order; out = full symmetric r x r fp64.
+ *   NMFB_F64: accumulated in fp64 (within 1e-14 of the BLAS Gram, matrix.py:181-197).
+ *   NMFB_F32: r % 4 == 0, 16 <= r <= 224, lda % 4 == 0, >= 2048 rows and a 16-byte
+ *     aligned A take the tcgen05 path (3xTF32 products, 64-row chunks folded
+ *     into round-to-nearest running sums, fp64 partials; within 1e-6 of the
+ *     exact Gram of the fp32 values); anything else sums 32-row fp32 slabs into
+ *     fp64 on the CUDA cores.  NMFB_GRAM_TC=0 in the environment forces the latter.
+ * workspace: nmfb_gram_workspace_bytes(rows, r) bytes of device memory. */
 size_t nmfb_gram_workspace_bytes(int64_t rows, int32_t r);
 /* Gram with the anti-lopsided rescale fused into its epilogue: out = A^T A
  * (as nmfb_gram), then Qa / scale_a / act_idx / active / ra_dev exactly as
